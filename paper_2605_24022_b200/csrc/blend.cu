@@ -1,0 +1,420 @@
+// (2)+(3) sparse gather + deferred RoPE + blend, and (4) QKV rope/scatter
+// epilogue.  Replaces ct/rope.py:42-81 (RopeParams.freqs / rope_rotate /
+// rope_apply), the reuse half of ct/pipesim.py:322-357 (fuse_layer), the
+// in-path gather of ct/toymodel.py:269-283 and the recompute half of
+// ct/toymodel.py:157-172.
+//
+// All kernels are HBM-bound row movers: one "unit" = VEC rotation pairs of
+// one head of one row (8 bf16 = 16 B per K/V access for adjacent pairing),
+// rows are walked grid-stride, and (cos, sin) comes from an L2-resident
+// [pos][D/2] table built once in float64 (F7: fp32 angles break at 64K).
+// fp32 mode (f32 caches) rotates in float64 with the unfused product/sum of
+// ct/rope.py:61-62 and rounds once to f32, reproducing the reference bits.
+#include "common.cuh"
+
+namespace ct {
+
+__global__ void rope_table_kernel(const double* __restrict__ freqs, int half, int64_t n_pos,
+                                  double scaling, const int64_t* __restrict__ positions,
+                                  double2* __restrict__ td, float2* __restrict__ tf) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= n_pos * half) return;
+  const int64_t p = positions ? positions[t / half] : t / half;
+  const int j = (int)(t % half);
+  // angles = outer(positions.astype(f64) * scaling, freqs)  (ct/rope.py:53-54)
+  const double ang = __dmul_rn(__dmul_rn((double)p, scaling), freqs[j]);
+  double s, c;
+  sincos(ang, &s, &c);
+  if (td) td[t] = make_double2(c, s);
+  if (tf) tf[t] = make_float2((float)c, (float)s);
+}
+
+// Rotate one group of VEC pairs.  a[i], b[i] are the pair members.
+template <int VEC>
+__device__ __forceinline__ void rotate_f64(float* a, float* b, const double2* cs) {
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const double x = a[i], y = b[i];
+    const double c = cs[i].x, s = cs[i].y;
+    const double ra = __dsub_rn(__dmul_rn(x, c), __dmul_rn(y, s));
+    const double rb = __dadd_rn(__dmul_rn(x, s), __dmul_rn(y, c));
+    a[i] = (float)ra;
+    b[i] = (float)rb;
+  }
+}
+template <int VEC>
+__device__ __forceinline__ void rotate_f32(float* a, float* b, const float2* cs) {
+#pragma unroll
+  for (int i = 0; i < VEC; ++i) {
+    const float x = a[i], y = b[i];
+    a[i] = x * cs[i].x - y * cs[i].y;
+    b[i] = x * cs[i].y + y * cs[i].x;
+  }
+}
+
+// Element offsets of pair group (head h, first pair j0) inside a row.
+// adjacent: elements 2j, 2j+1; split: j, j + D/2.
+template <typename T, int VEC>
+__device__ __forceinline__ void load_pairs(const T* row, int h, int j0, int D, int pairing,
+                                           float* a, float* b) {
+  const T* hp = row + (int64_t)h * D;
+  if (pairing == CT_ROPE_ADJACENT) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      a[i] = to_f32(hp[2 * (j0 + i)]);
+      b[i] = to_f32(hp[2 * (j0 + i) + 1]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      a[i] = to_f32(hp[j0 + i]);
+      b[i] = to_f32(hp[j0 + i + D / 2]);
+    }
+  }
+}
+template <typename T, int VEC>
+__device__ __forceinline__ void store_pairs(T* row, int h, int j0, int D, int pairing,
+                                            const float* a, const float* b) {
+  T* hp = row + (int64_t)h * D;
+  if (pairing == CT_ROPE_ADJACENT) {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      hp[2 * (j0 + i)] = from_f32<T>(a[i]);
+      hp[2 * (j0 + i) + 1] = from_f32<T>(b[i]);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) {
+      hp[j0 + i] = from_f32<T>(a[i]);
+      hp[j0 + i + D / 2] = from_f32<T>(b[i]);
+    }
+  }
+}
+
+// 16-byte vectorised specialisation for bf16 adjacent pairs (VEC = 4).
+__device__ __forceinline__ void load8_bf16(const __nv_bfloat16* p, float* a, float* b) {
+  const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h2[i]);
+    a[i] = f.x;
+    b[i] = f.y;
+  }
+}
+__device__ __forceinline__ void store8_bf16(__nv_bfloat16* p, const float* a, const float* b) {
+  uint4 u;
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) h2[i] = __floats2bfloat162_rn(a[i], b[i]);
+  *reinterpret_cast<uint4*>(p) = u;
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void rot_unit(const T* src, T* dst, int h, int j0, int D,
+                                         int pairing, const void* table, int64_t pos,
+                                         bool f64math) {
+  float a[VEC], b[VEC];
+  const int half = D / 2;
+  if constexpr (sizeof(T) == 2 && VEC == 4) {
+    if (pairing == CT_ROPE_ADJACENT) {
+      load8_bf16(reinterpret_cast<const __nv_bfloat16*>(src) + (int64_t)h * D + 2 * j0, a, b);
+    } else {
+      load_pairs<T, VEC>(src, h, j0, D, pairing, a, b);
+    }
+  } else {
+    load_pairs<T, VEC>(src, h, j0, D, pairing, a, b);
+  }
+  if (f64math) {
+    const double2* cs = reinterpret_cast<const double2*>(table) + pos * half + j0;
+    double2 c[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) c[i] = __ldg(cs + i);
+    rotate_f64<VEC>(a, b, c);
+  } else {
+    const float2* cs = reinterpret_cast<const float2*>(table) + pos * half + j0;
+    float2 c[VEC];
+#pragma unroll
+    for (int i = 0; i < VEC; ++i) c[i] = __ldg(cs + i);
+    rotate_f32<VEC>(a, b, c);
+  }
+  if constexpr (sizeof(T) == 2 && VEC == 4) {
+    if (pairing == CT_ROPE_ADJACENT) {
+      store8_bf16(reinterpret_cast<__nv_bfloat16*>(dst) + (int64_t)h * D + 2 * j0, a, b);
+      return;
+    }
+  }
+  store_pairs<T, VEC>(dst, h, j0, D, pairing, a, b);
+}
+
+template <typename T, int VEC>
+__device__ __forceinline__ void copy_unit(const T* src, T* dst, int h, int j0, int D,
+                                          int pairing) {
+  if constexpr (sizeof(T) == 2 && VEC == 4) {
+    if (pairing == CT_ROPE_ADJACENT) {
+      const int64_t o = (int64_t)h * D + 2 * j0;
+      *reinterpret_cast<uint4*>(dst + o) = __ldg(reinterpret_cast<const uint4*>(src + o));
+      return;
+    }
+  }
+  float a[VEC], b[VEC];
+  load_pairs<T, VEC>(src, h, j0, D, pairing, a, b);
+  store_pairs<T, VEC>(dst, h, j0, D, pairing, a, b);
+}
+
+struct SegArray {
+  ct_segment s[CT_MAX_SEGMENTS];
+};
+
+// grid: x = row blocks, y = segment.  256 threads; units per row = H*(D/2)/VEC.
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+gather_rope_blend_kernel(SegArray segs, int64_t src_row_stride, int H, int D, int pairing,
+                         const void* __restrict__ table, T* __restrict__ kc,
+                         T* __restrict__ vc, int64_t cache_row_stride, bool f64math) {
+  const ct_segment sg = segs.s[blockIdx.y];
+  const int upr = H * (D / 2) / VEC;  // units per row
+  const int64_t total = sg.rows * upr;
+  const T* ks = reinterpret_cast<const T*>(sg.k);
+  const T* vs = reinterpret_cast<const T*>(sg.v);
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = u / upr;
+    const int w = (int)(u % upr);
+    const int h = w / ((D / 2) / VEC);
+    const int j0 = (w % ((D / 2) / VEC)) * VEC;
+    const int32_t tk = __ldg(sg.tok + row);
+    const int64_t pos = sg.pos0 + tk;
+    const int64_t srow = sg.src_by_tok ? (int64_t)tk : row;
+    const T* ksrc = ks + srow * src_row_stride;
+    const T* vsrc = vs + srow * src_row_stride;
+    rot_unit<T, VEC>(ksrc, kc + pos * cache_row_stride, h, j0, D, pairing, table, pos, f64math);
+    copy_unit<T, VEC>(vsrc, vc + pos * cache_row_stride, h, j0, D, pairing);
+  }
+}
+
+template <typename T, int VEC>
+__global__ void __launch_bounds__(256)
+rope_apply_kernel(const T* __restrict__ x, const int32_t* __restrict__ positions, int64_t n,
+                  int H, int D, int pairing, const void* __restrict__ table, T* __restrict__ out,
+                  bool f64math) {
+  const int upr = H * (D / 2) / VEC;
+  const int64_t total = n * upr;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = u / upr;
+    const int w = (int)(u % upr);
+    const int h = w / ((D / 2) / VEC);
+    const int j0 = (w % ((D / 2) / VEC)) * VEC;
+    const int64_t pos = positions[row];
+    const int64_t ro = row * (int64_t)H * D;
+    rot_unit<T, VEC>(x + ro, out + ro, h, j0, D, pairing, table, pos, f64math);
+  }
+}
+
+// QKV epilogue.  Heads [0,Hq) -> q_out (rotated), [Hq, Hq+Hkv) -> k (rotated
+// into k_cache[pos], raw into k_raw_out[a]), [Hq+Hkv, Hq+2Hkv) -> v_cache[pos].
+template <typename TI, typename TQ, typename TC, int VEC>
+__global__ void __launch_bounds__(256)
+qkv_rope_scatter_kernel(const TI* __restrict__ qkv, int64_t ld_qkv,
+                        const int32_t* __restrict__ positions, int64_t A, int Hq, int Hkv, int D,
+                        int pairing, const void* __restrict__ table, TQ* __restrict__ q_out,
+                        TC* __restrict__ kc, TC* __restrict__ vc, int64_t cache_row_stride,
+                        TC* __restrict__ k_raw_out, bool f64math) {
+  const int hpr = Hq + 2 * Hkv;
+  const int gph = (D / 2) / VEC;
+  const int upr = hpr * gph;
+  const int64_t total = A * upr;
+  const int half = D / 2;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = u / upr;
+    const int w = (int)(u % upr);
+    const int hh = w / gph;
+    const int j0 = (w % gph) * VEC;
+    const int64_t pos = positions[a];
+    const TI* row = qkv + a * ld_qkv;
+    float x[VEC], y[VEC];
+    load_pairs<TI, VEC>(row, hh, j0, D, pairing, x, y);
+    if (hh >= Hq + Hkv) {  // value: copy
+      store_pairs<TC, VEC>(vc + pos * cache_row_stride, hh - Hq - Hkv, j0, D, pairing, x, y);
+      continue;
+    }
+    if (hh >= Hq && k_raw_out)
+      store_pairs<TC, VEC>(k_raw_out + a * (int64_t)Hkv * D, hh - Hq, j0, D, pairing, x, y);
+    if (f64math) {
+      const double2* cs = reinterpret_cast<const double2*>(table) + pos * half + j0;
+      double2 c[VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) c[i] = cs[i];
+      rotate_f64<VEC>(x, y, c);
+    } else {
+      const float2* cs = reinterpret_cast<const float2*>(table) + pos * half + j0;
+      float2 c[VEC];
+#pragma unroll
+      for (int i = 0; i < VEC; ++i) c[i] = cs[i];
+      rotate_f32<VEC>(x, y, c);
+    }
+    if (hh < Hq)
+      store_pairs<TQ, VEC>(q_out + a * (int64_t)Hq * D, hh, j0, D, pairing, x, y);
+    else
+      store_pairs<TC, VEC>(kc + pos * cache_row_stride, hh - Hq, j0, D, pairing, x, y);
+  }
+}
+
+__global__ void rows_copy_kernel(const uint32_t* __restrict__ src, const int32_t* __restrict__ idx,
+                                 int64_t n, int64_t words, uint32_t* __restrict__ dst,
+                                 bool scatter) {
+  const int64_t total = n * words;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = t / words, w = t % words;
+    const int64_t j = idx[i];
+    if (scatter)
+      dst[j * words + w] = src[i * words + w];
+    else
+      dst[i * words + w] = src[j * words + w];
+  }
+}
+
+static unsigned grid_for(int64_t units, int threads) {
+  int64_t b = (units + threads - 1) / threads;
+  const int64_t cap = 148 * 32;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+}  // namespace ct
+
+using namespace ct;
+
+extern "C" int ct_rope_table(const double* freqs, int64_t half_dim, int64_t n_pos,
+                             double scaling, const int64_t* positions, void* table_f64,
+                             void* table_f32, void* stream) {
+  if (half_dim < 1 || n_pos < 0) return fail(CT_ERR_SHAPE, "rope table geometry");
+  if (n_pos == 0) return CT_OK;
+  const int64_t total = half_dim * n_pos;
+  rope_table_kernel<<<(unsigned)((total + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+      freqs, (int)half_dim, n_pos, scaling, positions, (double2*)table_f64, (float2*)table_f32);
+  return check_launch("rope_table_kernel");
+}
+
+extern "C" int ct_rope_apply(const void* x, const int32_t* positions, int64_t n, int64_t H,
+                             int64_t D, int dtype, int pairing, const void* table, void* out,
+                             void* stream) {
+  if (D < 2 || D % 2) return fail(CT_ERR_SHAPE, "head_dim must be even, got %lld", (long long)D);
+  if (!valid_dtype(dtype)) return fail(CT_ERR_PARAM, "dtype %d", dtype);
+  if (pairing != CT_ROPE_ADJACENT && pairing != CT_ROPE_SPLIT) return fail(CT_ERR_PARAM, "pairing");
+  if (n == 0) return CT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool f64m = dtype == CT_F32;
+  const bool v4 = (D / 2) % 4 == 0;
+  const int64_t units = n * H * (D / 2) / (v4 ? 4 : 1);
+  const unsigned g = grid_for(units, 256);
+  if (dtype == CT_F32) {
+    if (v4) rope_apply_kernel<float, 4><<<g, 256, 0, st>>>((const float*)x, positions, n, (int)H, (int)D, pairing, table, (float*)out, f64m);
+    else rope_apply_kernel<float, 1><<<g, 256, 0, st>>>((const float*)x, positions, n, (int)H, (int)D, pairing, table, (float*)out, f64m);
+  } else {
+    if (v4) rope_apply_kernel<__nv_bfloat16, 4><<<g, 256, 0, st>>>((const __nv_bfloat16*)x, positions, n, (int)H, (int)D, pairing, table, (__nv_bfloat16*)out, f64m);
+    else rope_apply_kernel<__nv_bfloat16, 1><<<g, 256, 0, st>>>((const __nv_bfloat16*)x, positions, n, (int)H, (int)D, pairing, table, (__nv_bfloat16*)out, f64m);
+  }
+  return check_launch("rope_apply_kernel");
+}
+
+extern "C" int ct_gather_rope_blend(const ct_segment* segs, int n_segs, int64_t src_row_stride,
+                                    int64_t H, int64_t D, int dtype, int pairing,
+                                    const void* table, void* k_cache, void* v_cache,
+                                    int64_t cache_row_stride, void* stream) {
+  if (n_segs < 0 || n_segs > CT_MAX_SEGMENTS) return fail(CT_ERR_PARAM, "n_segs %d", n_segs);
+  if (D < 2 || D % 2) return fail(CT_ERR_SHAPE, "head_dim must be even");
+  if (!valid_dtype(dtype)) return fail(CT_ERR_PARAM, "dtype %d", dtype);
+  if (n_segs == 0) return CT_OK;
+  SegArray arr;
+  memset(&arr, 0, sizeof(arr));
+  int64_t max_rows = 0;
+  for (int i = 0; i < n_segs; ++i) {
+    arr.s[i] = segs[i];
+    if (segs[i].rows > max_rows) max_rows = segs[i].rows;
+  }
+  if (max_rows == 0) return CT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool v4 = (D / 2) % 4 == 0;
+  const int64_t upr = H * (D / 2) / (v4 ? 4 : 1);
+  int64_t bx = (max_rows * upr + 255) / 256;
+  const int64_t cap = (148 * 16 + n_segs - 1) / n_segs;
+  if (bx > cap) bx = cap;
+  dim3 grid((unsigned)bx, (unsigned)n_segs);
+  const bool f64m = dtype == CT_F32;
+  if (dtype == CT_F32) {
+    if (v4) gather_rope_blend_kernel<float, 4><<<grid, 256, 0, st>>>(arr, src_row_stride, (int)H, (int)D, pairing, table, (float*)k_cache, (float*)v_cache, cache_row_stride, f64m);
+    else gather_rope_blend_kernel<float, 1><<<grid, 256, 0, st>>>(arr, src_row_stride, (int)H, (int)D, pairing, table, (float*)k_cache, (float*)v_cache, cache_row_stride, f64m);
+  } else {
+    if (v4) gather_rope_blend_kernel<__nv_bfloat16, 4><<<grid, 256, 0, st>>>(arr, src_row_stride, (int)H, (int)D, pairing, table, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, cache_row_stride, f64m);
+    else gather_rope_blend_kernel<__nv_bfloat16, 1><<<grid, 256, 0, st>>>(arr, src_row_stride, (int)H, (int)D, pairing, table, (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache, cache_row_stride, f64m);
+  }
+  return check_launch("gather_rope_blend_kernel");
+}
+
+template <typename TI, typename TQ, typename TC, int VEC>
+static void launch_qkv(unsigned g, cudaStream_t st, const void* qkv, int64_t ld, const int32_t* pos,
+                       int64_t A, int Hq, int Hkv, int D, int pairing, const void* table,
+                       void* q_out, void* kc, void* vc, int64_t crs, void* kraw, bool f64m) {
+  qkv_rope_scatter_kernel<TI, TQ, TC, VEC><<<g, 256, 0, st>>>(
+      (const TI*)qkv, ld, pos, A, Hq, Hkv, D, pairing, table, (TQ*)q_out, (TC*)kc, (TC*)vc, crs,
+      (TC*)kraw, f64m);
+}
+
+extern "C" int ct_qkv_rope_scatter(const void* qkv, int64_t ld_qkv, int in_dtype,
+                                   const int32_t* positions, int64_t A, int64_t Hq, int64_t Hkv,
+                                   int64_t D, int pairing, const void* table, void* q_out,
+                                   int q_dtype, void* k_cache, void* v_cache, int cache_dtype,
+                                   int64_t cache_row_stride, void* k_raw_out, void* stream) {
+  if (D < 2 || D % 2) return fail(CT_ERR_SHAPE, "head_dim must be even");
+  if (Hkv < 1 || Hq % Hkv) return fail(CT_ERR_SHAPE, "Hq=%lld not a multiple of Hkv=%lld", (long long)Hq, (long long)Hkv);
+  if (!valid_dtype(in_dtype) || !valid_dtype(q_dtype) || !valid_dtype(cache_dtype))
+    return fail(CT_ERR_PARAM, "dtype");
+  if (A == 0) return CT_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool v4 = (D / 2) % 4 == 0;
+  const int64_t units = A * (Hq + 2 * Hkv) * (D / 2) / (v4 ? 4 : 1);
+  const unsigned g = grid_for(units, 256);
+  const bool f64m = cache_dtype == CT_F32;
+  const int key = in_dtype * 100 + q_dtype * 10 + cache_dtype;
+#define CT_QKV(TI, TQ, TC)                                                                       \
+  if (v4) launch_qkv<TI, TQ, TC, 4>(g, st, qkv, ld_qkv, positions, A, (int)Hq, (int)Hkv, (int)D, \
+                                    pairing, table, q_out, k_cache, v_cache, cache_row_stride,   \
+                                    k_raw_out, f64m);                                            \
+  else launch_qkv<TI, TQ, TC, 1>(g, st, qkv, ld_qkv, positions, A, (int)Hq, (int)Hkv, (int)D,    \
+                                 pairing, table, q_out, k_cache, v_cache, cache_row_stride,      \
+                                 k_raw_out, f64m);
+  switch (key) {
+    case CT_F32 * 100 + CT_F32 * 10 + CT_F32: CT_QKV(float, float, float) break;
+    case CT_BF16 * 100 + CT_BF16 * 10 + CT_BF16: CT_QKV(__nv_bfloat16, __nv_bfloat16, __nv_bfloat16) break;
+    case CT_F32 * 100 + CT_BF16 * 10 + CT_BF16: CT_QKV(float, __nv_bfloat16, __nv_bfloat16) break;
+    case CT_BF16 * 100 + CT_F32 * 10 + CT_F32: CT_QKV(__nv_bfloat16, float, float) break;
+    default: return fail(CT_ERR_UNSUPPORTED, "qkv dtype combination %d", key);
+  }
+#undef CT_QKV
+  return check_launch("qkv_rope_scatter_kernel");
+}
+
+extern "C" int ct_scatter_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
+                               void* dst, void* stream) {
+  if (row_bytes % 4) return fail(CT_ERR_PARAM, "row_bytes %% 4");
+  if (n == 0) return CT_OK;
+  const int64_t words = row_bytes / 4;
+  rows_copy_kernel<<<grid_for(n * words, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint32_t*)src, idx, n, words, (uint32_t*)dst, true);
+  return check_launch("rows_copy_kernel");
+}
+
+extern "C" int ct_gather_rows(const void* src, const int32_t* idx, int64_t n, int64_t row_bytes,
+                              void* dst, void* stream) {
+  if (row_bytes % 4) return fail(CT_ERR_PARAM, "row_bytes %% 4");
+  if (n == 0) return CT_OK;
+  const int64_t words = row_bytes / 4;
+  rows_copy_kernel<<<grid_for(n * words, 256), 256, 0, (cudaStream_t)stream>>>(
+      (const uint32_t*)src, idx, n, words, (uint32_t*)dst, false);
+  return check_launch("rows_copy_kernel");
+}

@@ -1,0 +1,162 @@
+// Transformer plumbing around the hot path: embedding gather
+// (ct/toymodel.py:149), fused residual add + RMSNorm (ct/toymodel.py:88-89,
+// :156, :184) and the MLP activation (ct/toymodel.py:186 ReLU; SwiGLU for the
+// Llama geometry).  Plus the library's version / error / transfer helpers.
+#include "common.cuh"
+
+namespace ct {
+
+thread_local char g_last_error[512] = "";
+
+__global__ void embedding_kernel(const float* __restrict__ table, const int32_t* __restrict__ tok,
+                                 int64_t A, int64_t cols, float* __restrict__ out) {
+  const int64_t total = A * cols;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = t / cols, c = t % cols;
+    out[t] = table[(int64_t)tok[a] * cols + c];
+  }
+}
+
+template <typename TD, typename TX>
+__global__ void __launch_bounds__(256)
+residual_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta, int64_t cols,
+                        double eps, TX* __restrict__ x) {
+  const int64_t row = blockIdx.x;
+  float* hr = h + row * cols;
+  const TD* dr = delta ? delta + row * cols : nullptr;
+  __shared__ double red[8];
+  double ss = 0.0;
+  for (int64_t c = threadIdx.x; c < cols; c += blockDim.x) {
+    float v = hr[c];
+    if (dr) {
+      v += to_f32(dr[c]);
+      hr[c] = v;
+    }
+    ss += (double)v * (double)v;
+  }
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    red[0] = t;
+  }
+  __syncthreads();
+  const float inv = (float)(1.0 / sqrt(red[0] / (double)cols + eps));
+  if (x)
+    for (int64_t c = threadIdx.x; c < cols; c += blockDim.x)
+      x[row * cols + c] = from_f32<TX>(hr[c] * inv);
+}
+
+template <typename TI, typename TO>
+__global__ void mlp_act_kernel(const TI* __restrict__ gu, int64_t A, int64_t inter, int kind,
+                               TO* __restrict__ act) {
+  const int64_t total = A * inter;
+  const int64_t ld = kind == 0 ? 2 * inter : inter;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = t / inter, i = t % inter;
+    const float g = to_f32(gu[a * ld + i]);
+    float r;
+    if (kind == 0) {
+      const float u = to_f32(gu[a * ld + inter + i]);
+      r = g / (1.f + expf(-g)) * u;
+    } else {
+      r = fmaxf(g, 0.f);
+    }
+    act[t] = from_f32<TO>(r);
+  }
+}
+
+static unsigned grid_cap(int64_t units) {
+  int64_t b = (units + 255) / 256;
+  if (b > 148 * 32) b = 148 * 32;
+  return (unsigned)(b < 1 ? 1 : b);
+}
+
+}  // namespace ct
+
+using namespace ct;
+
+extern "C" int ct_version(void) { return 1; }
+
+extern "C" int ct_last_error(char* buf, size_t len) {
+  if (!buf || !len) return CT_ERR_PARAM;
+  strncpy(buf, g_last_error, len - 1);
+  buf[len - 1] = 0;
+  return CT_OK;
+}
+
+extern "C" int ct_device_sm_count(void) {
+  int dev = 0, n = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return 0; }
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+extern "C" int ct_embedding_gather(const float* table, const int32_t* tokens, int64_t A,
+                                   int64_t cols, float* out, void* stream) {
+  if (A == 0) return CT_OK;
+  embedding_kernel<<<grid_cap(A * cols), 256, 0, (cudaStream_t)stream>>>(table, tokens, A, cols, out);
+  return check_launch("embedding_kernel");
+}
+
+extern "C" int ct_residual_rmsnorm(float* h, const void* delta, int delta_dtype, int64_t A,
+                                   int64_t cols, double eps, void* x_out, int x_dtype,
+                                   void* stream) {
+  if (A == 0) return CT_OK;
+  if (!valid_dtype(delta_dtype) || !valid_dtype(x_dtype)) return fail(CT_ERR_PARAM, "dtype");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned g = (unsigned)A;
+  if (delta_dtype == CT_F32 && x_dtype == CT_F32)
+    residual_rmsnorm_kernel<float, float><<<g, 256, 0, st>>>(h, (const float*)delta, cols, eps, (float*)x_out);
+  else if (delta_dtype == CT_F32 && x_dtype == CT_BF16)
+    residual_rmsnorm_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>(h, (const float*)delta, cols, eps, (__nv_bfloat16*)x_out);
+  else if (delta_dtype == CT_BF16 && x_dtype == CT_BF16)
+    residual_rmsnorm_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>(h, (const __nv_bfloat16*)delta, cols, eps, (__nv_bfloat16*)x_out);
+  else
+    residual_rmsnorm_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>(h, (const __nv_bfloat16*)delta, cols, eps, (float*)x_out);
+  return check_launch("residual_rmsnorm_kernel");
+}
+
+extern "C" int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype, int kind,
+                          void* act, int act_dtype, void* stream) {
+  if (A == 0) return CT_OK;
+  if (kind != 0 && kind != 1) return fail(CT_ERR_PARAM, "mlp kind %d", kind);
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned g = grid_cap(A * inter);
+  if (in_dtype == CT_F32 && act_dtype == CT_F32)
+    mlp_act_kernel<float, float><<<g, 256, 0, st>>>((const float*)gu, A, inter, kind, (float*)act);
+  else if (in_dtype == CT_BF16 && act_dtype == CT_BF16)
+    mlp_act_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, st>>>((const __nv_bfloat16*)gu, A, inter, kind, (__nv_bfloat16*)act);
+  else if (in_dtype == CT_F32 && act_dtype == CT_BF16)
+    mlp_act_kernel<float, __nv_bfloat16><<<g, 256, 0, st>>>((const float*)gu, A, inter, kind, (__nv_bfloat16*)act);
+  else
+    mlp_act_kernel<__nv_bfloat16, float><<<g, 256, 0, st>>>((const __nv_bfloat16*)gu, A, inter, kind, (float*)act);
+  return check_launch("mlp_act_kernel");
+}
+
+extern "C" int ct_copy_ranges_h2d(void* const* dst, const void* const* src, const int64_t* bytes,
+                                  int64_t n, void* stream) {
+  for (int64_t i = 0; i < n; ++i) {
+    if (bytes[i] <= 0) continue;
+    CT_CUDA(cudaMemcpyAsync(dst[i], src[i], (size_t)bytes[i], cudaMemcpyHostToDevice,
+                            (cudaStream_t)stream));
+  }
+  return CT_OK;
+}
+
+extern "C" int ct_host_alloc(void** ptr, size_t bytes) {
+  CT_CUDA(cudaHostAlloc(ptr, bytes, cudaHostAllocDefault));
+  return CT_OK;
+}
+
+extern "C" int ct_host_free(void* ptr) {
+  CT_CUDA(cudaFreeHost(ptr));
+  return CT_OK;
+}

@@ -1,0 +1,614 @@
+// (1) Frequency-domain critical-token scorer + deterministic ordering +
+// selection plan.  Replaces ct/spectral.py:69-90 (_band_scores /
+// low_freq_scores), :149-159 (rank_chunk), :99-101 (_descending_order),
+// :162-184 (selection) and the global assembly of ct/toymodel.py:246-267.
+//
+// Design (B200): the token axis of every (head, dim) lane is a real signal.
+// Two lanes are packed into one complex signal z = x_a + i x_b; because the
+// low-pass keeps a Hermitian-symmetric bin set, lowpass(z) = lowpass(x_a) +
+// i lowpass(x_b), so one complex FFT pair scores two lanes.  A CTA owns one
+// (chunk, layer, tensor, 128-lane block); it streams lane groups through a
+// shared-memory Stockham FFT (radix 8/4/2 passes, natural order, twiddles
+// from a float64 table), masks bins with min(k, N-k) >= c on the first
+// inverse pass, and accumulates |recon|^2 per token in registers across lane
+// groups.  Partial per-token energies of the lane blocks are combined in a
+// fixed order (deterministic), square-rooted, averaged over K/V and summed
+// sequentially over layers exactly as ct/spectral.py:74-78,156 do.  Orders
+// are a block bitonic sort on (score desc, index asc) == numpy's stable
+// argsort of -scores.  Non power-of-two N uses a direct circulant projection
+// (same math, O(N^2) per lane).
+#include "common.cuh"
+
+namespace ct {
+
+template <typename T> struct cpx { T x, y; };
+
+template <typename T>
+__device__ __forceinline__ cpx<T> cmul(cpx<T> a, cpx<T> b) {
+  return {a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ cpx<T> cadd(cpx<T> a, cpx<T> b) { return {a.x + b.x, a.y + b.y}; }
+template <typename T>
+__device__ __forceinline__ cpx<T> csub(cpx<T> a, cpx<T> b) { return {a.x - b.x, a.y - b.y}; }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV, typename T>
+__device__ __forceinline__ cpx<T> mul_mi(cpx<T> a) {
+  return INV ? cpx<T>{-a.y, a.x} : cpx<T>{a.y, -a.x};
+}
+
+template <int R, bool INV, typename T>
+__device__ __forceinline__ void dft_small(cpx<T>* v) {
+  if constexpr (R == 2) {
+    cpx<T> a = v[0], b = v[1];
+    v[0] = cadd(a, b);
+    v[1] = csub(a, b);
+  } else if constexpr (R == 4) {
+    cpx<T> t0 = cadd(v[0], v[2]), t1 = csub(v[0], v[2]);
+    cpx<T> t2 = cadd(v[1], v[3]), t3 = mul_mi<INV>(csub(v[1], v[3]));
+    v[0] = cadd(t0, t2);
+    v[2] = csub(t0, t2);
+    v[1] = cadd(t1, t3);
+    v[3] = csub(t1, t3);
+  } else {  // R == 8: radix-2 split into two radix-4 DFTs
+    cpx<T> e[4] = {v[0], v[2], v[4], v[6]};
+    cpx<T> o[4] = {v[1], v[3], v[5], v[7]};
+    dft_small<4, INV>(e);
+    dft_small<4, INV>(o);
+    const T h = (T)0.70710678118654752440;
+    // W8^k = exp(-/+ i pi k / 4)
+    cpx<T> w1 = INV ? cpx<T>{h, h} : cpx<T>{h, -h};
+    cpx<T> w3 = INV ? cpx<T>{-h, h} : cpx<T>{-h, -h};
+    cpx<T> o1 = cmul(o[1], w1);
+    cpx<T> o2 = mul_mi<INV>(o[2]);
+    cpx<T> o3 = cmul(o[3], w3);
+    v[0] = cadd(e[0], o[0]);
+    v[4] = csub(e[0], o[0]);
+    v[1] = cadd(e[1], o1);
+    v[5] = csub(e[1], o1);
+    v[2] = cadd(e[2], o2);
+    v[6] = csub(e[2], o2);
+    v[3] = cadd(e[3], o3);
+    v[7] = csub(e[3], o3);
+  }
+}
+
+template <typename T> struct ScoreCfg;
+// S complex signals (2S lanes) in flight per CTA; S*N*sizeof(cpx<T>) = 128 KiB.
+template <> struct ScoreCfg<double> { static constexpr int POINTS = 8192; };
+template <> struct ScoreCfg<float> { static constexpr int POINTS = 16384; };
+
+constexpr int SCORE_THREADS = 512;
+constexpr int LANE_BLOCK = 128;
+
+__host__ __device__ constexpr int pass_radix(int logn, int p) {
+  // radix-8 passes first, then one radix-4 or radix-2 pass for the rest
+  return (p < logn / 3) ? 8 : (1 << (logn % 3));
+}
+__host__ __device__ constexpr int num_passes(int logn) { return logn / 3 + (logn % 3 ? 1 : 0); }
+
+template <typename IN>
+__device__ __forceinline__ double load_as_double(const IN* p) { return (double)to_f32(*p); }
+__device__ __forceinline__ double load_as_double(const float* p) { return (double)*p; }
+
+// One Stockham pass over all S signals in shared memory (in place: every
+// thread loads all its butterflies, barrier, then stores).
+template <typename T, int LOGN, int R, bool INV, bool MASK>
+__device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
+                                              const cpx<T>* __restrict__ tw,
+                                              int cutoff) {
+  constexpr int N = 1 << LOGN;
+  constexpr int NB = N / R;  // butterflies per signal
+  constexpr int PTS = ScoreCfg<T>::POINTS;
+  constexpr int BPT = (PTS / R + SCORE_THREADS - 1) / SCORE_THREADS;
+  cpx<T> v[BPT][R];
+  const int total = S * NB;
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    const int b = threadIdx.x + k * SCORE_THREADS;
+    if (b < total) {
+      const int s = b / NB, j = b % NB;
+      const int jm = j % Ns;
+      const int step = N / (Ns * R);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int idx = j + r * NB;
+        cpx<T> val = sig[s * N + idx];
+        if (MASK) {
+          const int kk = idx < N - idx ? idx : N - idx;
+          if (kk >= cutoff) val = {(T)0, (T)0};
+        }
+        if (r > 0 && jm > 0) {
+          cpx<T> w = tw[jm * r * step];
+          if (INV) w.y = -w.y;
+          val = cmul(val, w);
+        }
+        v[k][r] = val;
+      }
+      dft_small<R, INV>(v[k]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < BPT; ++k) {
+    const int b = threadIdx.x + k * SCORE_THREADS;
+    if (b < total) {
+      const int s = b / NB, j = b % NB;
+      const int idxD = (j / Ns) * Ns * R + (j % Ns);
+#pragma unroll
+      for (int r = 0; r < R; ++r) sig[s * N + idxD + r * Ns] = v[k][r];
+    }
+  }
+  __syncthreads();
+}
+
+template <typename T, int LOGN, int P, bool INV, bool MASK_FIRST>
+__device__ __forceinline__ void run_passes(cpx<T>* sig, int S, int Ns,
+                                           const cpx<T>* tw, int cutoff) {
+  if constexpr (P < num_passes(LOGN) - (INV ? 1 : 0)) {
+    constexpr int R = pass_radix(LOGN, P);
+    stockham_pass<T, LOGN, R, INV, MASK_FIRST && P == 0>(sig, S, Ns, tw, cutoff);
+    run_passes<T, LOGN, P + 1, INV, MASK_FIRST>(sig, S, Ns * R, tw, cutoff);
+  }
+}
+
+template <int LOGN, int P>
+__host__ __device__ constexpr int ns_before() {
+  if constexpr (P == 0) return 1;
+  else return ns_before<LOGN, P - 1>() * pass_radix(LOGN, P - 1);
+}
+
+// grid: x = lane block, y = tensor (0 K, 1 V), z = c*L + l
+template <typename T, typename IN, int LOGN>
+__global__ void __launch_bounds__(SCORE_THREADS, 1)
+fft_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
+                  int L, int lanes, int64_t ld_token, int64_t ld_layer,
+                  int64_t ld_chunk, int cutoff, const cpx<T>* __restrict__ tw,
+                  double* __restrict__ partial) {
+  constexpr int N = 1 << LOGN;
+  constexpr int PTS = ScoreCfg<T>::POINTS;
+  constexpr int S = PTS / N < 1 ? 1 : (PTS / N > 64 ? 64 : PTS / N);
+  constexpr int NP = num_passes(LOGN);
+  constexpr int RL = pass_radix(LOGN, NP - 1);  // last pass radix
+  constexpr int NBL = N / RL;
+  constexpr int NSL = N / RL;                   // Ns of the last pass
+  constexpr int BPTL = (S * NBL + SCORE_THREADS - 1) / SCORE_THREADS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cpx<T>* sig = reinterpret_cast<cpx<T>*>(smem_raw);
+
+  const int lb = blockIdx.x, tensor = blockIdx.y;
+  const int c = blockIdx.z / L, l = blockIdx.z % L;
+  const IN* base = (tensor == 0 ? keys : values) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer;
+  const int lane0 = lb * LANE_BLOCK;
+  const int lane_end = min(lanes, lane0 + LANE_BLOCK);
+
+  double acc[BPTL][RL];
+#pragma unroll
+  for (int k = 0; k < BPTL; ++k)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) acc[k][r] = 0.0;
+
+  for (int g0 = lane0; g0 < lane_end; g0 += 2 * S) {
+    // load 2S lanes of every token; consecutive threads walk lanes then tokens
+    for (int q = threadIdx.x; q < S * N; q += SCORE_THREADS) {
+      const int s = q % S, n = q / S;
+      const int la = g0 + 2 * s, lbn = la + 1;
+      const IN* row = base + (int64_t)n * ld_token;
+      T re = la < lane_end ? (T)load_as_double(row + la) : (T)0;
+      T im = lbn < lane_end ? (T)load_as_double(row + lbn) : (T)0;
+      sig[s * N + n] = {re, im};
+    }
+    __syncthreads();
+    run_passes<T, LOGN, 0, false, false>(sig, S, 1, tw, cutoff);
+    run_passes<T, LOGN, 0, true, true>(sig, S, 1, tw, cutoff);
+    // last inverse pass: outputs go straight into per-token energy registers
+    {
+      constexpr int Ns = ns_before<LOGN, NP - 1>();
+      static_assert(Ns == NSL, "last pass span");
+#pragma unroll
+      for (int k = 0; k < BPTL; ++k) {
+        const int b = threadIdx.x + k * SCORE_THREADS;
+        if (b < S * NBL) {
+          const int s = b / NBL, j = b % NBL;
+          cpx<T> v[RL];
+#pragma unroll
+          for (int r = 0; r < RL; ++r) {
+            const int idx = j + r * NBL;
+            cpx<T> val = sig[s * N + idx];
+            if (NP == 1) {  // single pass: it is also the masked first pass
+              const int kk = idx < N - idx ? idx : N - idx;
+              if (kk >= cutoff) val = {(T)0, (T)0};
+            }
+            if (r > 0 && j > 0) {
+              cpx<T> w = tw[j * r * (N / (Ns * RL))];
+              w.y = -w.y;
+              val = cmul(val, w);
+            }
+            v[r] = val;
+          }
+          dft_small<RL, true>(v);
+#pragma unroll
+          for (int r = 0; r < RL; ++r)
+            acc[k][r] += (double)v[r].x * (double)v[r].x + (double)v[r].y * (double)v[r].y;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // combine signal slots in fixed order: E[s][token] then sum over s
+  double* E = reinterpret_cast<double*>(smem_raw);
+#pragma unroll
+  for (int k = 0; k < BPTL; ++k) {
+    const int b = threadIdx.x + k * SCORE_THREADS;
+    if (b < S * NBL) {
+      const int s = b / NBL, j = b % NBL;
+#pragma unroll
+      for (int r = 0; r < RL; ++r) E[s * N + j + r * NBL] = acc[k][r];
+    }
+  }
+  __syncthreads();
+  const double inv_n2 = 1.0 / ((double)N * (double)N);
+  const int nlb = gridDim.x;
+  double* out = partial + ((((int64_t)blockIdx.z * 2 + tensor) * nlb) + lb) * N;
+  for (int n = threadIdx.x; n < N; n += SCORE_THREADS) {
+    double e = 0.0;
+    for (int s = 0; s < S; ++s) e += E[s * N + n];
+    out[n] = e * inv_n2;
+  }
+}
+
+// Circulant low-pass kernel p[m] = (1/N)(1 + 2 sum_{k=1}^{kmax} cos(2 pi k m/N)
+// + nyq (-1)^m): the exact impulse response of rfft -> zero bins >= c -> irfft.
+__global__ void lowpass_kernel_table(int N, int cutoff, double* p) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= N) return;
+  if (cutoff <= 0) { p[m] = 0.0; return; }
+  const int kmax = min(cutoff - 1, (N - 1) / 2);
+  const bool nyq = (N % 2 == 0) && (cutoff >= N / 2 + 1);
+  double s = 1.0;
+  for (int k = 1; k <= kmax; ++k) {
+    const long long km = ((long long)k * m) % N;
+    s += 2.0 * cospi(2.0 * (double)km / (double)N);
+  }
+  if (nyq) s += (m & 1) ? -1.0 : 1.0;
+  p[m] = s / (double)N;
+}
+
+__global__ void twiddle_table(int N, cpx<double>* twd, cpx<float>* twf) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= N) return;
+  double s, c;
+  sincospi(2.0 * (double)m / (double)N, &s, &c);
+  if (twd) twd[m] = {c, -s};
+  if (twf) twf[m] = {(float)c, (float)-s};
+}
+
+// Direct path: y[i][lane] = sum_j p[(i-j) mod N] x[j][lane]; energy per token.
+// grid: x = token tile (32 tokens), y = tensor*nlb + lane block, z = c*L + l.
+template <typename IN>
+__global__ void __launch_bounds__(256)
+direct_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
+                     int N, int L, int lanes, int64_t ld_token, int64_t ld_layer,
+                     int64_t ld_chunk, const double* __restrict__ p, int nlb,
+                     double* __restrict__ partial) {
+  const int tensor = blockIdx.y / nlb, lb = blockIdx.y % nlb;
+  const int c = blockIdx.z / L, l = blockIdx.z % L;
+  const IN* base = (tensor == 0 ? keys : values) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer;
+  const int lane0 = lb * LANE_BLOCK, lane_end = min(lanes, lane0 + LANE_BLOCK);
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 warps x 4 tokens
+  __shared__ double red[8][4][33];
+  double energy[4] = {0, 0, 0, 0};
+  const int i0 = blockIdx.x * 32 + ty * 4;
+  for (int ls = lane0; ls < lane_end; ls += 32) {
+    const int lane = ls + tx;
+    double y[4] = {0, 0, 0, 0};
+    if (lane < lane_end) {
+      for (int j = 0; j < N; ++j) {
+        const double xv = load_as_double(base + (int64_t)j * ld_token + lane);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const int i = i0 + t;
+          if (i < N) {
+            int m = i - j;
+            m += (m < 0) ? N : 0;
+            y[t] += p[m] * xv;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) energy[t] += y[t] * y[t];
+  }
+  // fixed-order reduction over the 32 lanes of the warp
+#pragma unroll
+  for (int t = 0; t < 4; ++t) red[ty][t][tx] = energy[t];
+  __syncwarp();
+  if (tx < 4) {
+    double e = 0.0;
+    for (int q = 0; q < 32; ++q) e += red[ty][tx][q];
+    const int i = i0 + tx;
+    if (i < N)
+      partial[((((int64_t)blockIdx.z * 2 + tensor) * nlb) + lb) * N + i] = e;
+  }
+}
+
+// Per (chunk, token): layer score = 0.5*sqrt(EK) + 0.5*sqrt(EV); aggregate =
+// sequential layer sum / L (ct/spectral.py:74-78, :156).
+__global__ void combine_scores(const double* __restrict__ partial, int C, int L, int N,
+                               int nlb, double* __restrict__ layer_scores,
+                               double* __restrict__ agg) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= (int64_t)C * N) return;
+  const int c = (int)(t / N), n = (int)(t % N);
+  double total = 0.0;
+  for (int l = 0; l < L; ++l) {
+    double e[2];
+    for (int tensor = 0; tensor < 2; ++tensor) {
+      const double* src = partial + ((((int64_t)(c * L + l) * 2 + tensor) * nlb) * N) + n;
+      double s = 0.0;
+      for (int b = 0; b < nlb; ++b) s += src[(int64_t)b * N];
+      e[tensor] = s;
+    }
+    double score = 0.0;
+    score += 0.5 * sqrt(e[0]);
+    score += 0.5 * sqrt(e[1]);
+    layer_scores[((int64_t)c * L + l) * N + n] = score;
+    total += score;
+  }
+  if (agg) agg[t] = total / (double)L;
+}
+
+// Block bitonic sort of one row: descending score, ascending index on ties.
+constexpr int SORT_THREADS = 1024;
+__global__ void __launch_bounds__(SORT_THREADS)
+desc_order_kernel(const double* __restrict__ scores, int n, int P, int32_t* __restrict__ order) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* key = reinterpret_cast<double*>(smem_raw);
+  int* idx = reinterpret_cast<int*>(key + P);
+  const double* row = scores + (int64_t)blockIdx.x * n;
+  for (int i = threadIdx.x; i < P; i += SORT_THREADS) {
+    key[i] = i < n ? row[i] : -INFINITY;
+    idx[i] = i < n ? i : 0x7fffffff;
+  }
+  __syncthreads();
+  for (int k = 2; k <= P; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < P; i += SORT_THREADS) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const double ka = key[i], kb = key[ixj];
+          const int ia = idx[i], ib = idx[ixj];
+          // before(x, y): x.score > y.score || (== && x.idx < y.idx)
+          const bool b_before_a = (kb > ka) || (kb == ka && ib < ia);
+          const bool a_before_b = (ka > kb) || (ka == kb && ia < ib);
+          const bool asc = ((i & k) == 0);
+          if (asc ? b_before_a : a_before_b) {
+            key[i] = kb; key[ixj] = ka;
+            idx[i] = ib; idx[ixj] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  int32_t* out = order + (int64_t)blockIdx.x * n;
+  for (int i = threadIdx.x; i < n; i += SORT_THREADS) out[i] = idx[i];
+}
+
+// Selection plan: one CTA per chunk.  Marks the first k entries of the
+// aggregate order, then emits recomputed / kept tokens in ascending order
+// (ct/spectral.py:175-184) on the global axis (offset by the chunk start).
+constexpr int PLAN_THREADS = 1024;
+__global__ void __launch_bounds__(PLAN_THREADS)
+selection_plan_kernel(const int32_t* __restrict__ agg_orders, const int64_t* __restrict__ offsets,
+                      const int64_t* __restrict__ ks, const int64_t* __restrict__ rec_base,
+                      const int64_t* __restrict__ keep_base, int32_t* __restrict__ rec_global,
+                      int32_t* __restrict__ keep_global, int32_t* __restrict__ keep_src_row) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int c = blockIdx.x;
+  const int64_t off = offsets[c];
+  const int n = (int)(offsets[c + 1] - off);
+  const int k = (int)ks[c];
+  int* rank = reinterpret_cast<int*>(smem_raw);  // importance rank of each token
+  __shared__ int warp_tot[PLAN_THREADS / 32];
+  const int32_t* agg = agg_orders + off;
+  for (int i = threadIdx.x; i < n; i += PLAN_THREADS) rank[agg[i]] = i;
+  __syncthreads();
+  // contiguous segment per thread
+  const int per = (n + PLAN_THREADS - 1) / PLAN_THREADS;
+  const int t0 = threadIdx.x * per, t1 = min(n, t0 + per);
+  int cnt = 0;
+  for (int t = t0; t < t1; ++t) cnt += rank[t] < k;
+  // block exclusive scan of cnt
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int incl = cnt;
+  for (int d = 1; d < 32; d <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  if (lane == 31) warp_tot[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    int w = warp_tot[lane];
+    int wi = w;
+    for (int d = 1; d < 32; d <<= 1) {
+      int v = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= d) wi += v;
+    }
+    warp_tot[lane] = wi - w;
+  }
+  __syncthreads();
+  int rpos = warp_tot[warp] + incl - cnt;  // recomputed tokens before my segment
+  int kpos = t0 - rpos;                    // kept tokens before my segment
+  int32_t* rec = rec_global + rec_base[c];
+  int32_t* keep = keep_global + keep_base[c];
+  int32_t* ksrc = keep_src_row ? keep_src_row + keep_base[c] : nullptr;
+  for (int t = t0; t < t1; ++t) {
+    const int rk = rank[t];
+    if (rk < k) {
+      rec[rpos++] = (int32_t)(off + t);
+    } else {
+      if (ksrc) ksrc[kpos] = rk;
+      keep[kpos++] = (int32_t)(off + t);
+    }
+  }
+}
+
+static int ilog2_exact(int64_t n) {
+  if (n <= 0 || (n & (n - 1))) return -1;
+  int l = 0;
+  while ((1LL << l) < n) ++l;
+  return l;
+}
+
+static bool fft_path(int64_t N) {
+  const int lg = ilog2_exact(N);
+  return lg >= 3 && lg <= 13;
+}
+
+template <typename T, typename IN, int LOGN>
+static int launch_fft_t(const void* k, const void* v, int L, int C, int lanes, int64_t ldt,
+                        int64_t ldl, int64_t ldc, int cutoff, const void* tw,
+                        double* partial, cudaStream_t st) {
+  constexpr int N = 1 << LOGN;
+  constexpr int PTS = ScoreCfg<T>::POINTS;
+  constexpr int S = PTS / N < 1 ? 1 : (PTS / N > 64 ? 64 : PTS / N);
+  size_t smem = (size_t)S * N * sizeof(cpx<T>);
+  if (smem < (size_t)S * N * sizeof(double)) smem = (size_t)S * N * sizeof(double);
+  auto kern = fft_energy_kernel<T, IN, LOGN>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
+  dim3 grid(nlb, 2, C * L);
+  kern<<<grid, SCORE_THREADS, smem, st>>>((const IN*)k, (const IN*)v, L, lanes, ldt, ldl, ldc,
+                                          cutoff, (const cpx<T>*)tw, partial);
+  return check_launch("fft_energy_kernel");
+}
+
+template <typename T, typename IN>
+static int launch_fft(int logn, const void* k, const void* v, int L, int C, int lanes,
+                      int64_t ldt, int64_t ldl, int64_t ldc, int cutoff, const void* tw,
+                      double* partial, cudaStream_t st) {
+  switch (logn) {
+#define CT_CASE(LG) \
+  case LG: return launch_fft_t<T, IN, LG>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+    CT_CASE(3) CT_CASE(4) CT_CASE(5) CT_CASE(6) CT_CASE(7) CT_CASE(8) CT_CASE(9)
+    CT_CASE(10) CT_CASE(11) CT_CASE(12) CT_CASE(13)
+#undef CT_CASE
+    default: return fail(CT_ERR_UNSUPPORTED, "fft length 2^%d", logn);
+  }
+}
+
+}  // namespace ct
+
+using namespace ct;
+
+extern "C" size_t ct_score_workspace_bytes(int64_t C, int64_t L, int64_t N, int64_t lanes,
+                                           int precision) {
+  (void)precision;
+  const int64_t nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
+  size_t b = align_up((size_t)C * L * 2 * nlb * N * sizeof(double), 256);
+  b += align_up((size_t)N * sizeof(cpx<double>), 256);  // twiddles / circulant
+  b += align_up((size_t)N * sizeof(cpx<float>), 256);
+  return b;
+}
+
+extern "C" int ct_desc_order(const double* scores, int64_t rows, int64_t n, int32_t* order,
+                             void* stream) {
+  if (rows < 0 || n < 0) return fail(CT_ERR_SHAPE, "negative sizes");
+  if (rows == 0 || n == 0) return CT_OK;
+  int64_t P = 1;
+  while (P < n) P <<= 1;
+  const size_t smem = (size_t)P * (sizeof(double) + sizeof(int));
+  if (smem > 200 * 1024) return fail(CT_ERR_UNSUPPORTED, "order of %lld tokens exceeds one CTA", (long long)n);
+  CT_CUDA(cudaFuncSetAttribute(desc_order_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  desc_order_kernel<<<(unsigned)rows, SORT_THREADS, smem, (cudaStream_t)stream>>>(scores, (int)n, (int)P, order);
+  return check_launch("desc_order_kernel");
+}
+
+extern "C" int ct_score_chunks(const void* keys, const void* values, int dtype, int64_t C,
+                               int64_t L, int64_t N, int64_t lanes, int64_t ld_token,
+                               int64_t ld_layer, int64_t ld_chunk, int64_t cutoff, int precision,
+                               double* layer_scores, double* agg_scores, int32_t* layer_order,
+                               int32_t* agg_order, void* workspace, size_t workspace_bytes,
+                               void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (C < 1 || L < 1 || N < 1 || lanes < 1)
+    return fail(CT_ERR_SHAPE, "score geometry C=%lld L=%lld N=%lld lanes=%lld", (long long)C,
+                (long long)L, (long long)N, (long long)lanes);
+  if (!valid_dtype(dtype)) return fail(CT_ERR_PARAM, "dtype %d", dtype);
+  if (precision != CT_F64 && precision != CT_F32) return fail(CT_ERR_PARAM, "precision %d", precision);
+  if (cutoff < 0 || cutoff > N / 2 + 1) return fail(CT_ERR_PARAM, "cutoff %lld", (long long)cutoff);
+  if (!keys || !values || !layer_scores) return fail(CT_ERR_PARAM, "null tensor");
+  if (C * L > 65535) return fail(CT_ERR_UNSUPPORTED, "C*L too large");
+  if (workspace_bytes < ct_score_workspace_bytes(C, L, N, lanes, precision))
+    return fail(CT_ERR_PARAM, "workspace too small");
+  const int nlb = (int)((lanes + LANE_BLOCK - 1) / LANE_BLOCK);
+  char* ws = (char*)workspace;
+  double* partial = (double*)ws;
+  ws += align_up((size_t)C * L * 2 * nlb * N * sizeof(double), 256);
+  void* tw_d = ws;
+  ws += align_up((size_t)N * sizeof(cpx<double>), 256);
+  void* tw_f = ws;
+  int rc;
+  if (fft_path(N)) {
+    const int lg = ilog2_exact(N);
+    twiddle_table<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((int)N, (cpx<double>*)tw_d,
+                                                                (cpx<float>*)tw_f);
+    if ((rc = check_launch("twiddle_table"))) return rc;
+    if (precision == CT_F64) {
+      rc = dtype == CT_F32
+               ? launch_fft<double, float>(lg, keys, values, (int)L, (int)C, (int)lanes, ld_token,
+                                           ld_layer, ld_chunk, (int)cutoff, tw_d, partial, st)
+               : launch_fft<double, __nv_bfloat16>(lg, keys, values, (int)L, (int)C, (int)lanes,
+                                                   ld_token, ld_layer, ld_chunk, (int)cutoff, tw_d,
+                                                   partial, st);
+    } else {
+      rc = dtype == CT_F32
+               ? launch_fft<float, float>(lg, keys, values, (int)L, (int)C, (int)lanes, ld_token,
+                                          ld_layer, ld_chunk, (int)cutoff, tw_f, partial, st)
+               : launch_fft<float, __nv_bfloat16>(lg, keys, values, (int)L, (int)C, (int)lanes,
+                                                  ld_token, ld_layer, ld_chunk, (int)cutoff, tw_f,
+                                                  partial, st);
+    }
+    if (rc) return rc;
+  } else {
+    double* p = (double*)tw_d;
+    lowpass_kernel_table<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((int)N, (int)cutoff, p);
+    if ((rc = check_launch("lowpass_kernel_table"))) return rc;
+    dim3 grid((unsigned)((N + 31) / 32), (unsigned)(2 * nlb), (unsigned)(C * L));
+    if (dtype == CT_F32)
+      direct_energy_kernel<float><<<grid, 256, 0, st>>>((const float*)keys, (const float*)values,
+                                                        (int)N, (int)L, (int)lanes, ld_token,
+                                                        ld_layer, ld_chunk, p, nlb, partial);
+    else
+      direct_energy_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>(
+          (const __nv_bfloat16*)keys, (const __nv_bfloat16*)values, (int)N, (int)L, (int)lanes,
+          ld_token, ld_layer, ld_chunk, p, nlb, partial);
+    if ((rc = check_launch("direct_energy_kernel"))) return rc;
+  }
+  const int64_t total = C * N;
+  combine_scores<<<(unsigned)((total + 255) / 256), 256, 0, st>>>(partial, (int)C, (int)L, (int)N,
+                                                                  nlb, layer_scores, agg_scores);
+  if ((rc = check_launch("combine_scores"))) return rc;
+  if (layer_order && (rc = ct_desc_order(layer_scores, C * L, N, layer_order, stream))) return rc;
+  if (agg_order) {
+    if (!agg_scores) return fail(CT_ERR_PARAM, "agg_order needs agg_scores");
+    if ((rc = ct_desc_order(agg_scores, C, N, agg_order, stream))) return rc;
+  }
+  return CT_OK;
+}
+
+extern "C" int ct_selection_plan(const int32_t* agg_orders, const int64_t* offsets,
+                                 const int64_t* ks, const int64_t* rec_base,
+                                 const int64_t* keep_base, int64_t n_chunks,
+                                 int64_t max_chunk_tokens, int32_t* rec_global,
+                                 int32_t* keep_global, int32_t* keep_src_row, void* stream) {
+  if (n_chunks < 1) return fail(CT_ERR_PLAN, "need at least one chunk");
+  const size_t smem = (size_t)max_chunk_tokens * sizeof(int);
+  if (smem > 200 * 1024) return fail(CT_ERR_UNSUPPORTED, "chunk of %lld tokens", (long long)max_chunk_tokens);
+  CT_CUDA(cudaFuncSetAttribute(selection_plan_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  selection_plan_kernel<<<(unsigned)n_chunks, PLAN_THREADS, smem, (cudaStream_t)stream>>>(
+      agg_orders, offsets, ks, rec_base, keep_base, rec_global, keep_global, keep_src_row);
+  return check_launch("selection_plan_kernel");
+}

@@ -1,0 +1,347 @@
+"""(4) Selective-recompute prefill engine (drop-in for ct/toymodel.py:135-311).
+
+`selective_prefill` keeps the reference's signature, validation and result
+fields; `full_prefill` is the baseline and r=1 oracle; `encode_chunk_isolated`
+produces the pre-RoPE chunk KV (the offline producer).  Per layer the engine
+runs (all on the current CUDA stream, every op a libcachetune_b200 kernel
+except the dense projections, which are cuBLAS via torch.mm):
+
+  K4  ct_qkv_rope_scatter   q,k RoPE at active positions; k,v -> cache rows
+  K3  ct_gather_rope_blend  reused rows -> cache rows, K rotated at global pos
+  K5  ct_selective_attention  queries = active rows, keys = blended cache
+      ct_residual_rmsnorm / ct_mlp_act around the projections.
+"""
+
+from __future__ import annotations
+
+import math
+import threading
+from dataclasses import dataclass
+from typing import Callable, Sequence
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .errors import InvalidPlan, ShapeError
+from .kvcore import DeviceChunk, SeqTensor
+from .model import GpuModel
+from .rope import rope_table
+from .spectral import ImportanceRanking, select_device
+
+NORM_EPS = 1e-6  # ct/toymodel.py:28
+
+_models: dict = {}
+_models_lock = threading.Lock()
+
+
+def as_gpu_model(model, dtype=None) -> GpuModel:
+    """GpuModel as-is, or a (cached) upload of a reference ToyModel."""
+    if isinstance(model, GpuModel):
+        return model
+    dtype = dtype or torch.float32
+    key = (id(model), dtype)
+    with _models_lock:
+        hit = _models.get(key)
+        if hit is not None and hit[0] is model:
+            return hit[1]
+        dev = _dev.require_cuda()
+        g = GpuModel.from_reference(model, dtype=dtype, device=dev)
+        _models[key] = (model, g)
+        return g
+
+
+@dataclass(frozen=True)
+class AttentionRecord:
+    """Per-layer [n_heads, n_queries, n_context] attention (ct/toymodel.py:92-110)."""
+    matrices: tuple
+    query_positions: np.ndarray
+    n_context: int
+
+    def suffix_view(self, suffix_start: int) -> "AttentionRecord":
+        rows = np.flatnonzero(self.query_positions >= suffix_start)
+        mats = tuple(np.asarray(m)[:, rows, :suffix_start].copy() for m in self.matrices)
+        return AttentionRecord(mats, self.query_positions[rows].copy(), suffix_start)
+
+
+def attention_deviation(a: AttentionRecord, b: AttentionRecord) -> float:
+    """Mean Frobenius distance of two records (ct/toymodel.py:113-124)."""
+    if len(a.matrices) != len(b.matrices):
+        raise ShapeError("records have different layer counts")
+    total, count = 0.0, 0
+    for ma, mb in zip(a.matrices, b.matrices):
+        ma, mb = np.asarray(ma), np.asarray(mb)
+        if ma.shape != mb.shape:
+            raise ShapeError(f"attention shape mismatch {ma.shape} vs {mb.shape}")
+        for h in range(ma.shape[0]):
+            total += np.linalg.norm(ma[h] - mb[h])
+            count += 1
+    return float(total / count)
+
+
+@dataclass
+class PrefillResult:
+    """ct/toymodel.py:127-132; tensors stay on the device (see to_host)."""
+    kv: tuple                  # per layer (K post-RoPE, V), [n_ctx, H_kv, D] tensors
+    attention: AttentionRecord | None
+    logits: torch.Tensor       # [rows, vocab] f32
+    query_positions: np.ndarray
+
+    def to_host(self) -> "PrefillResult":
+        kv = tuple((SeqTensor(k.float().cpu().numpy()), SeqTensor(v.float().cpu().numpy()))
+                   for k, v in self.kv)
+        return PrefillResult(kv, self.attention, self.logits.double().cpu().numpy(),
+                             self.query_positions)
+
+
+def _auto_record(model: GpuModel, a: int, n_ctx: int, record) -> bool:
+    if record is not None:
+        return bool(record)
+    return model.config.n_heads * a * n_ctx <= (1 << 26)
+
+
+class LayerBuffers:
+    """Per-run activations (reused across layers)."""
+
+    def __init__(self, model: GpuModel, a: int, dev):
+        cfg = model.config
+        dt = model.dtype
+        hid, d = cfg.hidden_dim, cfg.head_dim
+        qkv = (cfg.n_heads + 2 * cfg.kv_heads) * d
+        self.h = torch.empty((a, hid), dtype=torch.float32, device=dev)
+        self.x = torch.empty((a, hid), dtype=dt, device=dev)
+        self.qkv = torch.empty((a, qkv), dtype=dt, device=dev)
+        self.q = torch.empty((a, cfg.n_heads, d), dtype=dt, device=dev)
+        self.ctx = torch.empty((a, cfg.n_heads * d), dtype=dt, device=dev)
+        width = {"relu": 4 * hid, "swiglu": 2 * cfg.inter}.get(cfg.mlp_kind, 0)
+        self.gu = torch.empty((a, width), dtype=dt, device=dev) if width else None
+        self.act = torch.empty((a, width // 2 if cfg.mlp_kind == "swiglu" else width),
+                               dtype=dt, device=dev) if width else None
+
+
+def _mm_f32(a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
+    if a.dtype == torch.float32:
+        return torch.mm(a, w)
+    return torch.mm(a, w, out_dtype=torch.float32)
+
+
+def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n_ctx: int,
+               caches: Sequence, reuse: Callable[[int], None] | None = None,
+               record_attention: bool = False, logits_rows: str | None = "all",
+               k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None):
+    """Shared forward engine (ct/toymodel.py:135-193) over device inputs.
+
+    tokens/positions: int32 [A] device.  caches[l] = (K, V) [n_ctx, Hkv, D]
+    (model dtype).  reuse(l) fills the reused rows of layer l before its
+    attention.  Returns (logits f32 [rows, V] or None, probs list)."""
+    cfg = model.config
+    dev = model.device
+    a = tokens.numel()
+    hid, hq, hkv, d = cfg.hidden_dim, cfg.n_heads, cfg.kv_heads, cfg.head_dim
+    dt = model.dtype
+    dtc = _dev.ct_dtype(dt)
+    st = _dev.stream_handle()
+    lib = _lib.load()
+    buf = buffers or LayerBuffers(model, a, dev)
+    params = cfg.rope_params
+    table = rope_table(params, n_ctx, "f64" if dt == torch.float32 else "f32", dev)
+    wsb = lib.ct_attention_workspace_bytes(a, hq, n_ctx, hkv, d, dtc)
+    ws = _dev.workspace(wsb, "attention")
+    scale = 1.0 / math.sqrt(d)
+    _lib.call("ct_embedding_gather", _dev.ptr(model.embedding), _dev.ptr(tokens), a, hid,
+              _dev.ptr(buf.h), st)
+    _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), None, _lib.CT_F32, a, hid, NORM_EPS,
+              _dev.ptr(buf.x), dtc, st)
+    probs_all = []
+    for l, w in enumerate(model.layers):
+        kc, vc = caches[l]
+        torch.mm(buf.x, w["wqkv"], out=buf.qkv)
+        _lib.check(lib.ct_qkv_rope_scatter(
+            _dev.ptr(buf.qkv), buf.qkv.shape[1], dtc, _dev.ptr(positions), a, hq, hkv, d,
+            params.pairing_code, _dev.ptr(table), _dev.ptr(buf.q), dtc, _dev.ptr(kc),
+            _dev.ptr(vc), dtc, hkv * d, _dev.ptr(k_raw_out[l]) if k_raw_out else None, st),
+            "ct_qkv_rope_scatter")
+        if reuse is not None:
+            reuse(l)
+        probs = (torch.empty((hq, a, n_ctx), dtype=torch.float32, device=dev)
+                 if record_attention else None)
+        _lib.check(lib.ct_selective_attention(
+            _dev.ptr(buf.q), _dev.ptr(positions), a, hq, _dev.ptr(kc), _dev.ptr(vc), n_ctx, hkv,
+            d, hkv * d, scale, dtc, _dev.ptr(buf.ctx), dtc, _dev.ptr(probs), _dev.ptr(ws), wsb,
+            st), "ct_selective_attention")
+        if record_attention:
+            probs_all.append(probs)
+        o = _mm_f32(buf.ctx, w["wo"])
+        _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), _dev.ptr(o), _lib.CT_F32, a, hid,
+                  NORM_EPS, _dev.ptr(buf.x), dtc, st)
+        kind = cfg.mlp_kind
+        if kind:
+            up = w["w1"] if kind == "relu" else w["wgu"]
+            down = w["w2"] if kind == "relu" else w["wd"]
+            torch.mm(buf.x, up, out=buf.gu)
+            inter = buf.act.shape[1]
+            _lib.call("ct_mlp_act", _dev.ptr(buf.gu), a, inter, dtc, 1 if kind == "relu" else 0,
+                      _dev.ptr(buf.act), dtc, st)
+            dlt = _mm_f32(buf.act, down)
+            _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), _dev.ptr(dlt), _lib.CT_F32, a,
+                      hid, NORM_EPS, _dev.ptr(buf.x), dtc, st)
+    logits = None
+    if logits_rows is not None and a:
+        hrows = buf.h if logits_rows == "all" else buf.h[-1:]
+        logits = _mm_f32(hrows.to(model.w_out.dtype), model.w_out)
+    return logits, probs_all
+
+
+def _check_tokens(model: GpuModel, toks: np.ndarray) -> None:
+    """ct/toymodel.py:81-85."""
+    if toks.ndim != 1 or toks.size < 1:
+        raise ShapeError("token ids must be a non-empty 1-d array")
+    if toks.min() < 0 or toks.max() >= model.config.vocab_size:
+        raise ShapeError("token id out of vocabulary")
+
+
+def _new_caches(model: GpuModel, n_ctx: int, dev):
+    cfg = model.config
+    return [(torch.empty((n_ctx, cfg.kv_heads, cfg.head_dim), dtype=model.dtype, device=dev),
+             torch.empty((n_ctx, cfg.kv_heads, cfg.head_dim), dtype=model.dtype, device=dev))
+            for _ in range(cfg.n_layers)]
+
+
+def full_prefill(model, tokens: Sequence[int], *, record_attention=None,
+                 logits_rows: str = "all", dtype=None) -> PrefillResult:
+    """Standard causal forward over the whole prompt (ct/toymodel.py:196-205)."""
+    g = as_gpu_model(model, dtype)
+    toks = np.asarray(tokens, dtype=np.int64)
+    _check_tokens(g, toks)
+    dev = g.device
+    n = toks.size
+    tok_d = torch.as_tensor(toks.astype(np.int32), device=dev)
+    pos_d = torch.arange(n, dtype=torch.int32, device=dev)
+    caches = _new_caches(g, n, dev)
+    rec = _auto_record(g, n, n, record_attention)
+    logits, probs = run_layers(g, tok_d, pos_d, n, caches, record_attention=rec,
+                               logits_rows=logits_rows)
+    att = (AttentionRecord(tuple(p.cpu().numpy() for p in probs), np.arange(n), n)
+           if rec else None)
+    return PrefillResult(tuple(caches), att, logits, np.arange(n))
+
+
+def encode_chunk_isolated(model, tokens: Sequence[int], chunk_id: str = "chunk", *,
+                          dtype=None) -> DeviceChunk:
+    """Forward the chunk alone at local positions; keep pre-RoPE K (ct/toymodel.py:208-220)."""
+    g = as_gpu_model(model, dtype)
+    toks = np.asarray(tokens, dtype=np.int64)
+    _check_tokens(g, toks)
+    cfg = g.config
+    dev = g.device
+    n = toks.size
+    shape = (cfg.n_layers, n, cfg.kv_heads, cfg.head_dim)
+    keys = torch.empty(shape, dtype=g.dtype, device=dev)
+    vals = torch.empty(shape, dtype=g.dtype, device=dev)
+    krot = torch.empty(shape[1:], dtype=g.dtype, device=dev)
+    caches = [(krot, vals[l]) for l in range(cfg.n_layers)]
+    tok_d = torch.as_tensor(toks.astype(np.int32), device=dev)
+    pos_d = torch.arange(n, dtype=torch.int32, device=dev)
+    run_layers(g, tok_d, pos_d, n, caches, logits_rows=None,
+               k_raw_out=[keys[l] for l in range(cfg.n_layers)])
+    return DeviceChunk(chunk_id, keys, vals, tok_d, toks)
+
+
+def _validate(cfg, chunks, rankings):
+    """ct/toymodel.py:234-244."""
+    if len(chunks) == 0 or len(chunks) != len(rankings):
+        raise InvalidPlan("need one ranking per chunk")
+    for chunk, ranking in zip(chunks, rankings):
+        if ranking.n_tokens != chunk.token_count:
+            raise InvalidPlan("ranking/chunk token counts disagree")
+        if chunk.n_layers != cfg.n_layers:
+            raise InvalidPlan("chunk layer count disagrees with model")
+        if (chunk.n_heads, chunk.head_dim) != (cfg.kv_heads, cfg.head_dim):
+            raise ShapeError("chunk geometry disagrees with model")
+        if chunk.source_tokens is None:
+            raise InvalidPlan("chunk lacks source_tokens; cannot recompute")
+
+
+def selective_prefill(model, chunks: Sequence, rankings: Sequence, suffix_tokens: Sequence[int],
+                      r: float, *, record_attention=None, logits_rows: str = "all",
+                      dtype=None) -> PrefillResult:
+    """Online reuse path (ct/toymodel.py:223-311): recompute the ratio-r
+    selection plus the suffix; every other token contributes its reused KV
+    through deferred-RoPE scatter fusion.  At r=1 this reproduces full_prefill."""
+    g = as_gpu_model(model, dtype)
+    cfg = g.config
+    _validate(cfg, chunks, rankings)
+    dev = g.device
+    dchunks = [c if isinstance(c, DeviceChunk) else DeviceChunk.from_host(c, g.dtype, dev)
+               for c in chunks]
+    for c in dchunks:
+        if c.keys.dtype != g.dtype:
+            raise ShapeError(f"chunk dtype {c.keys.dtype} != model dtype {g.dtype}")
+    sizes = [c.token_count for c in dchunks]
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    history = int(offsets[-1])
+    suffix = np.asarray(suffix_tokens, dtype=np.int64)
+    n_ctx = history + suffix.size
+    aggs = [rk.aggregate_device(dev) if isinstance(rk, ImportanceRanking)
+            else torch.as_tensor(np.asarray(rk.aggregate_order, np.int32), device=dev)
+            for rk in rankings]
+    rec, keep, _, ks = select_device(aggs, r, dev)
+    n_rec = rec.numel()
+    # active tokens = source tokens of the recomputed rows, then the suffix
+    src_all = torch.cat([c.tokens if c.tokens is not None else
+                         torch.as_tensor(np.asarray(c.source_tokens, np.int32), device=dev)
+                         for c in dchunks])
+    a = n_rec + suffix.size
+    positions = torch.empty(a, dtype=torch.int32, device=dev)
+    tokens = torch.empty(a, dtype=torch.int32, device=dev)
+    positions[:n_rec] = rec
+    if suffix.size:
+        positions[n_rec:] = torch.arange(history, n_ctx, dtype=torch.int32, device=dev)
+        tokens[n_rec:] = torch.as_tensor(suffix.astype(np.int32), device=dev)
+    if n_rec:
+        _lib.call("ct_gather_rows", _dev.ptr(src_all), _dev.ptr(rec), n_rec, 4,
+                  _dev.ptr(tokens), _dev.stream_handle())
+    qpos_host = positions.cpu().numpy().astype(np.int64)
+    if a:
+        # ct/toymodel.py:303 -- active token ids must be in the vocabulary
+        src_host = np.concatenate([np.asarray(c.source_tokens) for c in dchunks])
+        _check_tokens(g, np.concatenate([src_host[qpos_host[:n_rec]], suffix]))
+    caches = _new_caches(g, n_ctx, dev)
+    hkv, d = cfg.kv_heads, cfg.head_dim
+    keep_base = np.concatenate([[0], np.cumsum([n - k for n, k in zip(sizes, ks)])])
+    table = rope_table(cfg.rope_params, max(n_ctx, 1), "f64" if g.dtype == torch.float32
+                       else "f32", dev)
+    esize = torch.empty((), dtype=g.dtype).element_size()
+
+    def reuse(l: int) -> None:
+        segs = []
+        for j, c in enumerate(dchunks):
+            nk = int(keep_base[j + 1] - keep_base[j])
+            if nk == 0:
+                continue
+            # src row = global token - chunk offset: shift the base pointer
+            shift = int(offsets[j]) * hkv * d * esize
+            segs.append(_lib.Segment(_dev.ptr(c.keys[l]) - shift, _dev.ptr(c.values[l]) - shift,
+                                     _dev.ptr(keep) + int(keep_base[j]) * 4, nk, 0, 1))
+        kc, vc = caches[l]
+        for s0 in range(0, len(segs), _lib.CT_MAX_SEGMENTS):
+            part = segs[s0:s0 + _lib.CT_MAX_SEGMENTS]
+            arr = (_lib.Segment * len(part))(*part)
+            _lib.call("ct_gather_rope_blend", arr, len(part), hkv * d, hkv, d,
+                      _dev.ct_dtype(g.dtype), cfg.rope_params.pairing_code, _dev.ptr(table),
+                      _dev.ptr(kc), _dev.ptr(vc), hkv * d, _dev.stream_handle())
+
+    if a == 0:
+        for l in range(cfg.n_layers):
+            reuse(l)
+        att = AttentionRecord(tuple(np.zeros((cfg.n_heads, 0, n_ctx)) for _ in range(cfg.n_layers)),
+                              np.empty(0, np.int64), n_ctx)
+        return PrefillResult(tuple(caches), att,
+                             torch.zeros((0, cfg.vocab_size), dtype=torch.float32, device=dev),
+                             np.empty(0, np.int64))
+    rec_attn = _auto_record(g, a, n_ctx, record_attention)
+    logits, probs = run_layers(g, tokens, positions, n_ctx, caches, reuse=reuse,
+                               record_attention=rec_attn, logits_rows=logits_rows)
+    att = (AttentionRecord(tuple(p.cpu().numpy() for p in probs), qpos_host, n_ctx)
+           if rec_attn else None)
+    return PrefillResult(tuple(caches), att, logits, qpos_host)

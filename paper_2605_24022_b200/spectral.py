@@ -1,0 +1,245 @@
+"""(1) Frequency-domain critical-token scorer and ratio selection.
+
+Drop-in for ct/spectral.py: same names, argument order, defaults and errors.
+The arithmetic runs in libcachetune_b200.so (ct_score_chunks /
+ct_desc_order / ct_selection_plan); host code only validates arguments and
+moves results.  `precision="f64"` (default) scores with a float64 FFT like the
+reference's pocketfft so per-layer and aggregate orders are bit-exact;
+"f32" is the fast mode.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .errors import InvalidParam, ShapeError
+from .kvcore import DeviceChunk, KvChunk, SeqTensor
+
+DEFAULT_ALPHA = 0.5  # ct/spectral.py:24
+
+
+def cutoff_index(alpha: float, n_freqs: int) -> int:
+    """c = floor(alpha * n_freqs) as a float product (ct/spectral.py:57-58)."""
+    return int(math.floor(alpha * n_freqs))
+
+
+def _check_alpha(alpha: float) -> None:
+    if not 0.0 <= alpha <= 1.0:
+        raise InvalidParam(f"alpha must be in [0, 1], got {alpha}")
+
+
+def selection_count(r: float, n_tokens: int) -> int:
+    """ceil(r*N - 1e-9) clamped to [0, N] (ct/spectral.py:162-172)."""
+    if not 0.0 <= r <= 1.0:
+        raise InvalidParam(f"ratio must be in [0, 1], got {r}")
+    k = math.ceil(r * n_tokens - 1e-9)
+    return min(max(k, 0), n_tokens)
+
+
+@dataclass(frozen=True)
+class ImportanceRanking:
+    """Descending token permutations (ct/spectral.py:104-146).
+
+    Host arrays as in the reference; `device_aggregate` (optional) keeps the
+    aggregate order resident in HBM as int32 for the online path."""
+
+    per_layer_scores: np.ndarray
+    per_layer_order: np.ndarray
+    aggregate_order: np.ndarray
+    alpha: float
+    n_tokens: int
+    device_aggregate: object = None
+
+    def __post_init__(self):
+        scores = np.asarray(self.per_layer_scores, dtype=np.float64)
+        orders = np.asarray(self.per_layer_order, dtype=np.int64)
+        agg = np.asarray(self.aggregate_order, dtype=np.int64)
+        if scores.ndim != 2 or scores.shape != orders.shape:
+            raise ShapeError("per-layer scores/orders must be [L, N] and congruent")
+        n = self.n_tokens
+        if scores.shape[1] != n or agg.shape != (n,):
+            raise ShapeError("ranking arrays disagree with n_tokens")
+        want = np.arange(n)
+        if not np.array_equal(np.sort(agg), want):
+            raise InvalidParam("aggregate_order is not a permutation of [0, N)")
+        for row in orders:
+            if not np.array_equal(np.sort(row), want):
+                raise InvalidParam("per-layer order is not a permutation of [0, N)")
+        if not np.all(np.isfinite(scores)) or (scores.size and scores.min() < 0):
+            raise InvalidParam("scores must be finite and >= 0")
+        for name, arr in (("per_layer_scores", scores), ("per_layer_order", orders),
+                          ("aggregate_order", agg)):
+            arr = np.ascontiguousarray(arr)
+            arr.flags.writeable = False
+            object.__setattr__(self, name, arr)
+
+    @property
+    def n_layers(self) -> int:
+        return self.per_layer_scores.shape[0]
+
+    def aggregate_device(self, device) -> torch.Tensor:
+        d = self.device_aggregate
+        if d is not None and d.device == torch.device(device):
+            return d
+        return torch.as_tensor(self.aggregate_order.astype(np.int32), device=device)
+
+
+def _as_device_kv(keys, values):
+    """Accept SeqTensor-likes, numpy [N,H,D] or torch tensors [L?,N,H,D]."""
+    dev = _dev.require_cuda()
+
+    def conv(x):
+        if isinstance(x, torch.Tensor):
+            return x.to(dev)
+        data = x.data if hasattr(x, "data") and not isinstance(x, np.ndarray) else x
+        return torch.from_numpy(np.ascontiguousarray(np.asarray(data, dtype=np.float32))).to(dev)
+    k, v = conv(keys), conv(values)
+    if k.dim() == 3:
+        k, v = k.unsqueeze(0), v.unsqueeze(0)
+    return k, v
+
+
+def score_device(keys: torch.Tensor, values: torch.Tensor, alpha: float = DEFAULT_ALPHA,
+                 precision: str = "f64", want_layer_order: bool = True):
+    """Score C chunks on the device.
+
+    keys/values: [C, L, N, H, D] (or [L, N, H, D]) f32/bf16 CUDA tensors.
+    Returns dict of device tensors: layer_scores [C,L,N] f64, agg [C,N] f64,
+    layer_order [C,L,N] int32 (optional), agg_order [C,N] int32."""
+    _check_alpha(alpha)
+    if keys.shape != values.shape:
+        raise ShapeError(f"keys {tuple(keys.shape)} vs values {tuple(values.shape)}")
+    if keys.dim() == 4:
+        keys, values = keys.unsqueeze(0), values.unsqueeze(0)
+    if keys.dim() != 5:
+        raise ShapeError("expected [C, L, N, H, D]")
+    keys, values = keys.contiguous(), values.contiguous()
+    C, L, N, H, D = keys.shape
+    lanes = H * D
+    dev = keys.device
+    cutoff = cutoff_index(alpha, N // 2 + 1)
+    prec = _lib.CT_F64 if precision == "f64" else _lib.CT_F32
+    out = {
+        "layer_scores": torch.empty((C, L, N), dtype=torch.float64, device=dev),
+        "agg": torch.empty((C, N), dtype=torch.float64, device=dev),
+        "agg_order": torch.empty((C, N), dtype=torch.int32, device=dev),
+        "layer_order": (torch.empty((C, L, N), dtype=torch.int32, device=dev)
+                        if want_layer_order else None),
+    }
+    lib = _lib.load()
+    wsb = lib.ct_score_workspace_bytes(C, L, N, lanes, prec)
+    ws = _dev.workspace(wsb, "score")
+    _lib.check(lib.ct_score_chunks(
+        _dev.ptr(keys), _dev.ptr(values), _dev.ct_dtype(keys.dtype), C, L, N, lanes,
+        lanes, N * lanes, L * N * lanes, cutoff, prec,
+        _dev.ptr(out["layer_scores"]), _dev.ptr(out["agg"]), _dev.ptr(out["layer_order"]),
+        _dev.ptr(out["agg_order"]), _dev.ptr(ws), wsb, _dev.stream_handle()), "ct_score_chunks")
+    return out
+
+
+def low_freq_scores(keys, values, alpha: float = DEFAULT_ALPHA,
+                    precision: str = "f64") -> np.ndarray:
+    """Per-token importance (ct/spectral.py:82-90): 0.5|K~_i| + 0.5|V~_i|."""
+    _check_alpha(alpha)
+    ks = getattr(keys, "shape", None)
+    vs = getattr(values, "shape", None)
+    if tuple(ks) != tuple(vs):
+        raise ShapeError(f"keys {ks} vs values {vs}")
+    k, v = _as_device_kv(keys, values)
+    out = score_device(k, v, alpha, precision, want_layer_order=False)
+    return out["layer_scores"][0, 0].cpu().numpy()
+
+
+def _chunk_tensors(chunk):
+    if isinstance(chunk, DeviceChunk):
+        return chunk.keys, chunk.values
+    dev = _dev.require_cuda()
+    k = np.stack([np.asarray(t.data, dtype=np.float32) for t in chunk.keys_raw])
+    v = np.stack([np.asarray(t.data, dtype=np.float32) for t in chunk.values])
+    return torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev)
+
+
+def rank_chunk(chunk, alpha: float = DEFAULT_ALPHA, precision: str = "f64") -> ImportanceRanking:
+    """Score every layer and build the importance permutations (ct/spectral.py:149-159)."""
+    _check_alpha(alpha)
+    k, v = _chunk_tensors(chunk)
+    out = score_device(k, v, alpha, precision)
+    n = k.shape[1]
+    return ImportanceRanking(
+        per_layer_scores=out["layer_scores"][0].cpu().numpy(),
+        per_layer_order=out["layer_order"][0].cpu().numpy().astype(np.int64),
+        aggregate_order=out["agg_order"][0].cpu().numpy().astype(np.int64),
+        alpha=alpha, n_tokens=n, device_aggregate=out["agg_order"][0])
+
+
+def rank_chunks(chunks, alpha: float = DEFAULT_ALPHA, precision: str = "f64",
+                host: bool = True):
+    """Batched rank_chunk over equal-geometry device chunks (one launch set)."""
+    keys = torch.stack([c.keys for c in chunks])
+    vals = torch.stack([c.values for c in chunks])
+    out = score_device(keys, vals, alpha, precision, want_layer_order=host)
+    if not host:
+        return out
+    res = []
+    ls, lo, ao = (out["layer_scores"].cpu().numpy(), out["layer_order"].cpu().numpy(),
+                  out["agg_order"].cpu().numpy())
+    for i in range(len(chunks)):
+        res.append(ImportanceRanking(per_layer_scores=ls[i], per_layer_order=lo[i].astype(np.int64),
+                                     aggregate_order=ao[i].astype(np.int64), alpha=alpha,
+                                     n_tokens=keys.shape[2], device_aggregate=out["agg_order"][i]))
+    return res
+
+
+def select_device(agg_orders: list, ratios, device=None):
+    """Device selection plan over chunks laid end to end (ct/spectral.py:175-184,
+    ct/toymodel.py:246-260).  agg_orders: list of device int32 [N_j] tensors.
+    Returns (rec_global int32 ascending, keep_global int32 ascending,
+    keep_src_row int32 importance ranks, ks list)."""
+    device = device or agg_orders[0].device
+    if np.isscalar(ratios):
+        ratios = [ratios] * len(agg_orders)
+    sizes = [int(a.numel()) for a in agg_orders]
+    ks = [selection_count(r, n) for r, n in zip(ratios, sizes)]
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    rec_base = np.concatenate([[0], np.cumsum(ks)]).astype(np.int64)
+    keep_base = np.concatenate([[0], np.cumsum([n - k for n, k in zip(sizes, ks)])]).astype(np.int64)
+    meta = torch.as_tensor(np.concatenate([offsets, np.asarray(ks, np.int64), rec_base,
+                                           keep_base]), device=device)
+    nc = len(sizes)
+    off_d = meta[: nc + 1]
+    ks_d = meta[nc + 1: 2 * nc + 1]
+    rb_d = meta[2 * nc + 1: 3 * nc + 2]
+    kb_d = meta[3 * nc + 2:]
+    aggs = torch.cat([a.to(torch.int32) for a in agg_orders])
+    rec = torch.empty(int(rec_base[-1]), dtype=torch.int32, device=device)
+    keep = torch.empty(int(keep_base[-1]), dtype=torch.int32, device=device)
+    ksrc = torch.empty_like(keep)
+    _lib.call("ct_selection_plan", _dev.ptr(aggs), _dev.ptr(off_d), _dev.ptr(ks_d),
+              _dev.ptr(rb_d), _dev.ptr(kb_d), nc, max(sizes), _dev.ptr(rec), _dev.ptr(keep),
+              _dev.ptr(ksrc), _dev.stream_handle())
+    return rec, keep, ksrc, ks
+
+
+def indices_for_ratio(ranking, r: float) -> np.ndarray:
+    """First ceil(r*N) tokens of the aggregate order, ascending (ct/spectral.py:175-178)."""
+    selection_count(r, ranking.n_tokens)  # validates r
+    dev = _dev.require_cuda()
+    agg = (ranking.aggregate_device(dev) if isinstance(ranking, ImportanceRanking)
+           else torch.as_tensor(np.asarray(ranking.aggregate_order, np.int32), device=dev))
+    rec, _, _, _ = select_device([agg], r, dev)
+    return rec.cpu().numpy().astype(np.int64)
+
+
+def complement_for_ratio(ranking, r: float) -> np.ndarray:
+    """Tokens NOT selected at ratio r, ascending (ct/spectral.py:181-184)."""
+    selection_count(r, ranking.n_tokens)
+    dev = _dev.require_cuda()
+    agg = (ranking.aggregate_device(dev) if isinstance(ranking, ImportanceRanking)
+           else torch.as_tensor(np.asarray(ranking.aggregate_order, np.int32), device=dev))
+    _, keep, _, _ = select_device([agg], r, dev)
+    return keep.cpu().numpy().astype(np.int64)

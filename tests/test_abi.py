@@ -1,0 +1,66 @@
+"""C-ABI library: builds, loads without a GPU and exports every symbol the
+header declares.  CPU only (no compute calls)."""
+
+import ctypes
+import re
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+HEADER = ROOT / "include" / "cachetune_b200.h"
+
+
+def header_symbols():
+    text = HEADER.read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(ct_[a-z0-9_]+)\s*\(", text)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2605_24022_b200 import _build, _lib
+    _build.build()
+    return _lib.load()
+
+
+def test_header_declares_entry_points():
+    syms = header_symbols()
+    for want in ("ct_score_chunks", "ct_selection_plan", "ct_gather_rope_blend",
+                 "ct_qkv_rope_scatter", "ct_selective_attention", "ct_copy_ranges_h2d"):
+        assert want in syms
+
+
+def test_library_exports_every_header_symbol(lib):
+    for name in header_symbols():
+        assert hasattr(lib, name), name
+
+
+def test_binding_covers_header(lib):
+    from paper_2605_24022_b200 import _lib
+    assert set(header_symbols()) == set(_lib.EXPORTS)
+
+
+def test_version_and_error_plumbing(lib):
+    from paper_2605_24022_b200 import _lib
+    assert lib.ct_version() >= 1
+    # a pure argument error is reported without touching the device
+    st = lib.ct_desc_order(None, -1, 4, None, None)
+    assert st == 1
+    with pytest.raises(_lib.ShapeError):
+        _lib.check(st, "ct_desc_order")
+
+
+def test_workspace_query_is_host_only(lib):
+    n = lib.ct_score_workspace_bytes(16, 32, 2048, 1024, 2)
+    assert n >= 16 * 32 * 2 * 8 * 2048 * 8
+
+
+def test_sass_is_sm100a():
+    lib_path = ROOT / "paper_2605_24022_b200" / "libcachetune_b200.so"
+    if not lib_path.exists():
+        pytest.skip("library not built")
+    import subprocess
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", str(lib_path)],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out

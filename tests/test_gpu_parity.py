@@ -1,0 +1,338 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle and the
+golden fixtures produced by the live reference.
+
+Tolerances (stated per north_star): selected-token index sets and orders are
+bit-exact; blended K/V and logits are normwise max|d|/max|ref| <= 1e-5 in the
+fp32 mode and <= 2e-2 in the bf16 mode.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+from oracle import cachetune_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+FP32_TOL = 1e-5
+BF16_TOL = 2e-2
+
+
+@pytest.fixture(scope="module")
+def ct():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_24022_b200 as ct
+    from paper_2605_24022_b200 import _lib
+    _lib.load()
+    return ct
+
+
+def _bf16_round(x: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+
+
+# ---------------------------------------------------------------- scorer
+
+def test_spectral_cases_bit_exact(ct):
+    g = golden("spectral_cases")
+    for i in range(int(g["count"])):
+        keys, vals, alpha = g[f"c{i}_keys"], g[f"c{i}_vals"], float(g[f"c{i}_alpha"])
+        chunk = ct.KvChunk("c", tuple(ct.SeqTensor(k) for k in keys),
+                           tuple(ct.SeqTensor(v) for v in vals))
+        rk = ct.rank_chunk(chunk, alpha)
+        want = g[f"c{i}_scores"]
+        np.testing.assert_allclose(rk.per_layer_scores, want, rtol=1e-11,
+                                   atol=1e-13 * max(1.0, float(np.max(want))), err_msg=str(i))
+        assert np.array_equal(rk.aggregate_order, g[f"c{i}_agg"]), i
+        assert np.array_equal(rk.per_layer_order, g[f"c{i}_orders"]), i
+        for r, tag in ((0.15, "sel15"), (0.05, "sel05"), (0.5, "sel50")):
+            assert np.array_equal(ct.indices_for_ratio(rk, r), g[f"c{i}_{tag}"]), (i, r)
+
+
+def _big(seed, geom):
+    l, n, h, d = geom
+    rng = np.random.default_rng(seed)
+    keys = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(l)]
+    vals = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(l)]
+    return keys, vals
+
+
+@pytest.mark.parametrize("precision", ["f64", "f32"])
+def test_big_chunks_config2_geometry(ct, precision):
+    """[2048, 8, 128] chunks (config-2 layer geometry), f32 and bf16 inputs."""
+    g = golden("big_chunks")
+    from paper_2605_24022_b200.spectral import score_device
+    for s in g["seeds"]:
+        keys, vals = _big(int(s), g["geometry"])
+        k = torch.from_numpy(np.stack(keys)).cuda()
+        v = torch.from_numpy(np.stack(vals)).cuda()
+        out = score_device(k, v, 0.5, precision)
+        sc = out["layer_scores"][0].cpu().numpy()
+        rel = np.max(np.abs(sc - g[f"s{s}_scores"]) / g[f"s{s}_scores"])
+        if precision == "f64":
+            assert rel < 1e-12
+            assert np.array_equal(out["agg_order"][0].cpu().numpy(), g[f"s{s}_agg"])
+            assert np.array_equal(out["layer_order"][0].cpu().numpy(), g[f"s{s}_orders"])
+        else:
+            assert rel < 1e-6
+            kk = O.selection_count(0.15, 2048)
+            got = np.sort(out["agg_order"][0].cpu().numpy()[:kk])
+            assert np.array_equal(got, np.sort(g[f"s{s}_agg"][:kk].astype(np.int64)))
+        # bf16-resident KV: score the bf16 values (reference scored the same rounding)
+        outb = score_device(k.to(torch.bfloat16), v.to(torch.bfloat16), 0.5, "f64")
+        assert np.array_equal(outb["agg_order"][0].cpu().numpy(), g[f"s{s}_bf16_agg"])
+
+
+def test_batched_chunks_and_selection_plan(ct):
+    from paper_2605_24022_b200.spectral import score_device, select_device
+    rng = np.random.default_rng(7)
+    C, L, N, H, D = 5, 3, 512, 2, 16
+    k = torch.from_numpy(rng.standard_normal((C, L, N, H, D)).astype(np.float32)).cuda()
+    v = torch.from_numpy(rng.standard_normal((C, L, N, H, D)).astype(np.float32)).cuda()
+    out = score_device(k, v)
+    aggs = []
+    for c in range(C):
+        _, _, agg = O.rank_chunk(list(k[c].cpu().numpy()), list(v[c].cpu().numpy()))
+        assert np.array_equal(out["agg_order"][c].cpu().numpy(), agg)
+        aggs.append(agg)
+    for r in (0.0, 0.15, 0.37, 1.0):
+        rec, keep, ksrc, ks = select_device([out["agg_order"][c] for c in range(C)], r)
+        want_rec = np.concatenate([O.indices_for_ratio(a, r) + c * N for c, a in enumerate(aggs)])
+        want_keep = np.concatenate([O.complement_for_ratio(a, r) + c * N
+                                    for c, a in enumerate(aggs)])
+        assert np.array_equal(rec.cpu().numpy(), want_rec)
+        assert np.array_equal(keep.cpu().numpy(), want_keep)
+        # keep_src_row = importance rank of each kept token
+        kg = keep.cpu().numpy()
+        ranks = np.concatenate([np.argsort(a) for a in aggs])
+        assert np.array_equal(ksrc.cpu().numpy(), ranks[kg])
+
+
+# ---------------------------------------------------------------- rope / fuse
+
+def test_rope_cases_bit_exact(ct):
+    g = golden("rope_cases")
+    for i in range(int(g["count"])):
+        d, base, scaling, pairing = g[f"r{i}_params"]
+        p = ct.RopeParams(int(d), float(base), float(scaling),
+                          "adjacent" if int(pairing) == 0 else "split")
+        y = ct.rope_apply(ct.SeqTensor(g[f"r{i}_x"]), g[f"r{i}_pos"], p).data
+        want = g[f"r{i}_y"]
+        ulp = np.abs(y.view(np.int32).astype(np.int64) - want.view(np.int32).astype(np.int64))
+        assert ulp.max() <= 1, i  # cos/sin from CUDA vs numpy libm: <= 1 ulp after rounding
+        assert np.mean(ulp == 0) > 0.999, i
+
+
+def test_rope_inverse_and_negative_positions(ct):
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((7, 2, 8)).astype(np.float32)
+    pos = rng.integers(0, 500, size=7)
+    p = ct.RopeParams(head_dim=8)
+    fwd = ct.rope_apply(ct.SeqTensor(x), pos, p)
+    back = ct.rope_apply(fwd, -pos, p)
+    assert np.max(np.abs(back.data - x)) < 1e-6
+
+
+def test_fuse_cases(ct):
+    g = golden("fuse_cases")
+    for i in range(int(g["count"])):
+        f = lambda k: g[f"f{i}_{k}"]
+        keep, rec = f("keep"), f("rec")
+        d = f("kr").shape[2] if keep.size else f("kn").shape[2]
+        K, V = ct.fuse_layer(
+            (ct.SeqTensor(f("kr")) if keep.size else None,
+             ct.SeqTensor(f("vr")) if keep.size else None, keep),
+            (ct.SeqTensor(f("kn")) if rec.size else None,
+             ct.SeqTensor(f("vn")) if rec.size else None, rec),
+            positions=keep, rope_params=ct.RopeParams(head_dim=d), n=keep.size + rec.size)
+        assert np.array_equal(V.data, f("V"))
+        assert np.max(np.abs(K.data - f("K"))) <= 1e-6 * np.max(np.abs(f("K")))
+
+
+def test_fuse_rejects_bad_partition(ct):
+    x = ct.SeqTensor(np.ones((6, 2, 4), np.float32))
+    with pytest.raises(ct.InvalidPlan):
+        ct.fuse_layer((x, x, np.arange(6)), (x, x, np.array([5])), np.arange(6),
+                      ct.RopeParams(head_dim=4), 6)
+
+
+# ---------------------------------------------------------------- attention kernel
+
+def _torch_attention(q, pos, k, v, hq, hkv):
+    """Plain PyTorch fp32 reference of ct/toymodel.py:176-183 with GQA."""
+    a, _, d = q.shape
+    n = k.shape[0]
+    g = hq // hkv
+    kk = k.float().repeat_interleave(g, dim=1).permute(1, 2, 0)   # [H, D, n]
+    vv = v.float().repeat_interleave(g, dim=1).permute(1, 0, 2)   # [H, n, D]
+    s = torch.bmm(q.float().permute(1, 0, 2), kk) / d ** 0.5       # [H, A, n]
+    mask = torch.arange(n, device=q.device)[None, :] <= pos[:, None].long()
+    s = s.masked_fill(~mask[None], float("-inf"))
+    p = torch.softmax(s, dim=-1)
+    return torch.bmm(p, vv).permute(1, 0, 2), p
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16])
+@pytest.mark.parametrize("geom", [(37, 4, 2, 8, 300), (300, 32, 8, 128, 2500),
+                                  (129, 8, 8, 64, 777)])
+def test_attention_kernel_vs_torch(ct, dtype, geom):
+    from paper_2605_24022_b200 import _dev, _lib
+    a, hq, hkv, d, n = geom
+    gen = torch.Generator(device="cuda").manual_seed(11)
+    q = torch.randn((a, hq, d), device="cuda", generator=gen).to(dtype)
+    k = torch.randn((n, hkv, d), device="cuda", generator=gen).to(dtype)
+    v = torch.randn((n, hkv, d), device="cuda", generator=gen).to(dtype)
+    pos = torch.sort(torch.randperm(n, device="cuda", generator=gen)[:a])[0].to(torch.int32)
+    pos[-1] = n - 1
+    out = torch.empty((a, hq, d), device="cuda", dtype=dtype)
+    lib = _lib.load()
+    wsb = lib.ct_attention_workspace_bytes(a, hq, n, hkv, d, _dev.ct_dtype(dtype))
+    ws = _dev.workspace(wsb, "t")
+    _lib.call("ct_selective_attention", _dev.ptr(q), _dev.ptr(pos), a, hq, _dev.ptr(k),
+              _dev.ptr(v), n, hkv, d, hkv * d, 1.0 / d ** 0.5, _dev.ct_dtype(dtype),
+              _dev.ptr(out), _dev.ct_dtype(dtype), None, _dev.ptr(ws), wsb,
+              _dev.stream_handle())
+    want, _ = _torch_attention(q, pos, k, v, hq, hkv)
+    err = (out.float() - want).abs().max().item() / want.abs().max().item()
+    assert err < (2e-6 if dtype == torch.float32 else 1e-2), err
+
+
+def test_attention_probs_record(ct):
+    from paper_2605_24022_b200 import _dev, _lib
+    a, hq, hkv, d, n = 20, 2, 2, 8, 70
+    gen = torch.Generator(device="cuda").manual_seed(5)
+    q = torch.randn((a, hq, d), device="cuda", generator=gen)
+    k = torch.randn((n, hkv, d), device="cuda", generator=gen)
+    v = torch.randn((n, hkv, d), device="cuda", generator=gen)
+    pos = torch.randint(0, n, (a,), device="cuda", generator=gen).to(torch.int32)
+    out = torch.empty_like(q)
+    probs = torch.empty((hq, a, n), device="cuda")
+    _lib.call("ct_selective_attention", _dev.ptr(q), _dev.ptr(pos), a, hq, _dev.ptr(k),
+              _dev.ptr(v), n, hkv, d, hkv * d, 1.0 / d ** 0.5, 0, _dev.ptr(out), 0,
+              _dev.ptr(probs), None, 0, _dev.stream_handle())
+    want_o, want_p = _torch_attention(q, pos, k, v, hq, hkv)
+    assert (probs - want_p).abs().max().item() < 1e-6
+    assert (out - want_o).abs().max().item() < 1e-5
+
+
+# ---------------------------------------------------------------- config 1 end to end
+
+def _cfg1_inputs(ct, g, tag):
+    chunks, ranks = [], []
+    for j in range(4):
+        keys, vals = g[f"{tag}_chunk{j}_keys"], g[f"{tag}_chunk{j}_vals"]
+        c = ct.KvChunk(f"c{j}", tuple(ct.SeqTensor(k) for k in keys),
+                       tuple(ct.SeqTensor(v) for v in vals), source_tokens=g[f"{tag}_tokens"][j])
+        chunks.append(c)
+        ranks.append(ct.rank_chunk(c))
+    return chunks, ranks
+
+
+@pytest.mark.parametrize("tag,mlp", [("cfg1", False), ("cfg1mlp", True)])
+def test_config1_selective_prefill_vs_reference(ct, tag, mlp):
+    g = golden("toy_cfg1")
+    model = O.Model(O.ModelConfig(seed=0, n_layers=2, mlp=mlp))
+    chunks, ranks = _cfg1_inputs(ct, g, tag)
+    for j, rk in enumerate(ranks):
+        assert np.array_equal(rk.aggregate_order, g[f"{tag}_chunk{j}_agg"])
+    res = ct.selective_prefill(model, chunks, ranks, g[f"{tag}_suffix"], 0.15)
+    assert np.array_equal(res.query_positions, g[f"{tag}_qpos"])
+    logits = res.logits.double().cpu().numpy()
+    assert O.normwise_rel(logits, g[f"{tag}_logits"]) < FP32_TOL
+    assert O.normwise_rel(logits[-1], g[f"{tag}_logits"][-1]) < FP32_TOL
+    for l in range(2):
+        K, V = res.kv[l]
+        assert O.normwise_rel(K.cpu().numpy(), g[f"{tag}_kv{l}_k"]) < FP32_TOL
+        assert O.normwise_rel(V.cpu().numpy(), g[f"{tag}_kv{l}_v"]) < FP32_TOL
+    sv = res.attention.suffix_view(2048)
+    for l in range(2):
+        got = sv.matrices[l][:, -4:, :]
+        assert O.normwise_rel(got, g[f"{tag}_attn{l}_suffix"]) < FP32_TOL
+
+
+def test_config1_r1_matches_full_and_r0_pure_reuse(ct):
+    g = golden("toy_cfg1")
+    model = O.Model(O.ModelConfig(seed=0, n_layers=2))
+    chunks, ranks = _cfg1_inputs(ct, g, "cfg1")
+    suffix = g["cfg1_suffix"]
+    full = ct.full_prefill(model, np.concatenate([g["cfg1_tokens"].reshape(-1), suffix]))
+    assert O.normwise_rel(full.logits[-1].double().cpu().numpy(),
+                          g["cfg1_full_logits_last"]) < FP32_TOL
+    sel1 = ct.selective_prefill(model, chunks, ranks, suffix, 1.0)
+    assert np.max(np.abs(sel1.logits[-1].double().cpu().numpy()
+                         - full.logits[-1].double().cpu().numpy())) < 1e-5
+    assert O.normwise_rel(sel1.logits[-1].double().cpu().numpy(),
+                          g["cfg1_r1_logits_last"]) < FP32_TOL
+    sel0 = ct.selective_prefill(model, chunks, ranks, suffix, 0.0)
+    assert O.normwise_rel(sel0.logits[-1].double().cpu().numpy(),
+                          g["cfg1_r0_logits_last"]) < FP32_TOL
+    # r=0 without suffix: pure reuse, K = rope_apply(stored K) bit-exact
+    pure = ct.selective_prefill(model, chunks, ranks, [], 0.0)
+    assert pure.logits.shape[0] == 0
+    K0 = pure.kv[0][0].cpu().numpy()
+    want = ct.rope_apply(chunks[1].keys_raw[0], np.arange(512, 1024),
+                         ct.RopeParams(head_dim=8)).data
+    assert np.array_equal(K0[512:1024], want)
+
+
+def test_selective_validates_inputs(ct):
+    g = golden("toy_cfg1")
+    model = O.Model(O.ModelConfig(seed=0, n_layers=2))
+    chunks, ranks = _cfg1_inputs(ct, g, "cfg1")
+    with pytest.raises(ct.InvalidPlan):
+        ct.selective_prefill(model, chunks, ranks[:2], [1, 2], 0.15)
+    with pytest.raises(ct.InvalidPlan):
+        ct.selective_prefill(model, [], [], [1, 2], 0.15)
+    with pytest.raises(ct.InvalidParam):
+        ct.selective_prefill(model, chunks, ranks, [1, 2], 1.5)
+    bare = ct.KvChunk("b", chunks[0].keys_raw, chunks[0].values)
+    with pytest.raises(ct.InvalidPlan):
+        ct.selective_prefill(model, [bare], ranks[:1], [1], 0.15)
+    with pytest.raises(ct.ShapeError):
+        ct.selective_prefill(model, chunks, ranks, [999], 0.15)
+
+
+def test_encode_chunk_isolated_matches_oracle(ct):
+    model = O.Model(O.ModelConfig(seed=3, n_layers=3, mlp=True))
+    toks = np.random.default_rng(0).integers(0, 256, size=77)
+    kr, vs = O.encode_chunk_isolated(model, toks)
+    dc = ct.encode_chunk_isolated(model, toks)
+    for l in range(3):
+        assert O.normwise_rel(dc.keys[l].cpu().numpy(), kr[l]) < FP32_TOL
+        assert O.normwise_rel(dc.values[l].cpu().numpy(), vs[l]) < FP32_TOL
+
+
+# ---------------------------------------------------------------- Llama geometry, bf16 mode
+
+def test_llama_geometry_bf16_reduced(ct):
+    """Config-2 geometry (GQA 32/8, D=128, SwiGLU) at 2 layers / 2 x 2048 chunks /
+    S=64 in bf16 mode vs the float64 oracle on identical (bf16-valued) inputs."""
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=2048, seed=1)
+    gm = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(2)
+    toks = [rng.integers(0, 2048, size=2048) for _ in range(2)]
+    suffix = rng.integers(0, 2048, size=64)
+    chunks = [ct.encode_chunk_isolated(gm, t, chunk_id=f"c{j}") for j, t in enumerate(toks)]
+    ranks = [ct.rank_chunk(c) for c in chunks]
+    res = ct.selective_prefill(gm, chunks, ranks, suffix, 0.15, logits_rows="last")
+    # oracle on the same weights / chunk KV values
+    w = gm.to_numpy_weights()
+    ocfg = O.ModelConfig(seed=1, n_layers=2, n_heads=32, head_dim=128, vocab_size=2048,
+                         mlp="swiglu", n_kv_heads=8, intermediate=14336)
+    om = O.Model(ocfg, weights=w)
+    och = [([c.keys[l].float().cpu().numpy() for l in range(2)],
+            [c.values[l].float().cpu().numpy() for l in range(2)], t)
+           for c, t in zip(chunks, toks)]
+    aggs = [O.rank_chunk(kr, vs)[2] for kr, vs, _ in och]
+    for rk, agg in zip(ranks, aggs):
+        assert np.array_equal(rk.aggregate_order, agg)
+    want = O.selective_prefill(om, och, aggs, suffix, 0.15, want_probs=False,
+                               logits_rows="last")
+    got = res.logits.double().cpu().numpy()
+    assert O.normwise_rel(got, want["logits"]) < BF16_TOL
+    for l in range(2):
+        K, V = res.kv[l]
+        assert O.normwise_rel(K.float().cpu().numpy(), want["kv"][l][0]) < BF16_TOL
+        assert O.normwise_rel(V.float().cpu().numpy(), want["kv"][l][1]) < BF16_TOL
