@@ -1,12 +1,514 @@
-// (4) selective-recompute attention on tcgen05/TMEM (bf16 operands, fp32
-// accumulation).  Placeholder until the tensor-core kernel lands.
+// (4) Selective-recompute attention on the 5th-gen tensor cores (sm_100a):
+// tcgen05.mma with fp32 accumulators in TMEM, bf16 operands staged by TMA.
+// Replaces the attention of ct/toymodel.py:176-183 (q = selected rows + suffix
+// at global positions, keys/values = the full blended cache, key j visible to
+// a query iff j <= its position).
+//
+// Tile = 128 TMEM lanes = (128/G queries) x (G q-heads of one kv-head), so a
+// K/V tile staged once serves the whole GQA group.  Per 128-key block:
+//   S = Q K^T      tcgen05.mma  M128 N128 K16 x8, A=Q smem, B=K smem -> TMEM
+//   softmax        one thread per row: tcgen05.ld S row, mask by position,
+//                  exp2, lazy max (rescale O only when the max grows > 2^8),
+//                  P (bf16) written swizzled to smem
+//   O += P V       tcgen05.mma  M128 N128 K16 x8, A=P smem, B=V smem (MN-major)
+// Warp roles: warps 0-3 softmax/epilogue (TMEM lanes 0-127), warp 4 TMA
+// producer, warp 5 MMA issuer (+TMEM alloc).  S is double buffered in TMEM,
+// P double buffered in smem, K/V flow through a 3-slot TMA ring.
 #include "common.cuh"
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 namespace ct {
-bool tc_enabled() { return false; }
-size_t attention_tc_workspace(int64_t, int64_t, int64_t, int64_t, int64_t) { return 0; }
-int attention_tc(const void*, const int32_t*, int64_t, int64_t, const void*, const void*, int64_t,
-                 int64_t, int64_t, int64_t, double, void*, int, void*, size_t, cudaStream_t) {
-  return fail(CT_ERR_UNSUPPORTED, "tcgen05 attention not built");
+
+namespace tc {
+
+constexpr int TILE_M = 128;   // TMEM lanes / MMA M
+constexpr int BLK_N = 128;    // keys per block
+constexpr int HD = 128;       // head dim
+constexpr int KV_SLOTS = 3;
+constexpr int THREADS = 192;
+constexpr int ATOM_BYTES = 128 * 64 * 2;      // [128 rows][64 bf16] swizzle-128B half tile
+constexpr int TILE_BYTES = 2 * ATOM_BYTES;    // 32 KiB: 128 rows x 128 bf16
+constexpr float LAZY_THRESH = 8.0f;           // log2 units
+
+struct Smem {
+  // offsets from the 1024-aligned base
+  static constexpr int Q = 0;
+  static constexpr int KV = Q + TILE_BYTES;
+  static constexpr int P = KV + KV_SLOTS * TILE_BYTES;
+  static constexpr int BAR = P + 2 * TILE_BYTES;
+  static constexpr int NBAR = 16;
+  static constexpr int TMEM_PTR = BAR + NBAR * 8;
+  static constexpr int TOTAL = TMEM_PTR + 16;
+};
+
+__device__ __forceinline__ uint32_t su32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
 }
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+// 32 consecutive TMEM columns of this thread's lane.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t* r) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+        "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+        "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+// wait::ld, threading the registers through so uses cannot move above it
+__device__ __forceinline__ void tmem_wait_ld32(uint32_t* r) {
+  asm volatile(
+      "tcgen05.wait::ld.sync.aligned;"
+      : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]),
+        "+r"(r[7]), "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]),
+        "+r"(r[14]), "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]),
+        "+r"(r[20]), "+r"(r[21]), "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]),
+        "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
+      :
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
+      "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
+      "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() {
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor, SWIZZLE_128B (sm100 version bit set).
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;          // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;          // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::f16, bf16 A/B, f32 D, M=128, N=128.
+__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
+         ((uint32_t)(BLK_N >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+}
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+struct Params {
+  const int32_t* qpos;
+  __nv_bfloat16* out;
+  float* out_f32;
+  int A, Hq, Hkv, G, QB;  // G = Hq/Hkv rows per query, QB = 128/G queries per tile
+  int n_ctx;
+  int n_qblocks;
+  float scale_log2;
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
+                    const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const Params p) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sQ = base + Smem::Q, sKV = base + Smem::KV, sP = base + Smem::P;
+  uint8_t* gP = gbase + Smem::P;
+  const uint32_t bar0 = base + Smem::BAR;
+  // barriers
+  const uint32_t bar_q = bar0 + 0 * 8;
+  auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };            // 3
+  auto bar_empty = [&](int s) { return bar0 + (4 + s) * 8; };           // 3
+  auto bar_sfull = [&](int b) { return bar0 + (7 + b) * 8; };           // 2
+  auto bar_sempty = [&](int b) { return bar0 + (9 + b) * 8; };          // 2
+  auto bar_pfull = [&](int b) { return bar0 + (11 + b) * 8; };          // 2
+  auto bar_pempty = [&](int b) { return bar0 + (13 + b) * 8; };         // 2
+  const uint32_t bar_odone = bar0 + 15 * 8;
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + Smem::TMEM_PTR);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // longest tiles first: high query blocks (largest positions) get low block ids
+  const int tile = blockIdx.x;
+  const int qb = p.n_qblocks - 1 - (tile / p.Hkv);
+  const int g = tile % p.Hkv;
+  const int a0 = qb * p.QB;
+
+  int maxpos = 0;
+  for (int i = 0; i < p.QB; ++i) {
+    const int a = a0 + i;
+    if (a < p.A) maxpos = max(maxpos, __ldg(p.qpos + a));
+  }
+  maxpos = min(maxpos, p.n_ctx - 1);
+  const int nb = maxpos / BLK_N + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < KV_SLOTS; ++s) {
+      mbar_init(bar_full(s), 1);
+      mbar_init(bar_empty(s), 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar_sfull(b), 1);
+      mbar_init(bar_sempty(b), 128);
+      mbar_init(bar_pfull(b), 128);
+      mbar_init(bar_pempty(b), 1);
+    }
+    mbar_init(bar_odone, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_ptr)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_ptr;
+  const uint32_t tS[2] = {tbase + 0, tbase + 128};
+  const uint32_t tO = tbase + 256;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(bar_q, TILE_BYTES);
+      tma_load_3d(sQ, &map_q, bar_q, 0, g * p.G, a0);
+      tma_load_3d(sQ + ATOM_BYTES, &map_q, bar_q, 64, g * p.G, a0);
+      int slot = 0;
+      uint32_t phase = 0;
+      auto load = [&](const CUtensorMap* m, int j) {
+        mbar_wait(bar_empty(slot), phase ^ 1);
+        const uint32_t dst = sKV + slot * TILE_BYTES;
+        mbar_expect_tx(bar_full(slot), TILE_BYTES);
+        tma_load_3d(dst, m, bar_full(slot), 0, g, j * BLK_N);
+        tma_load_3d(dst + ATOM_BYTES, m, bar_full(slot), 64, g, j * BLK_N);
+        if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
+      };
+      // same order the MMA warp consumes: K0, K1, V0, K2, V1, ...
+      load(&map_k, 0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) load(&map_k, j + 1);
+        load(&map_v, j);
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = idesc_bf16(false);
+      constexpr uint32_t IDESC_O = idesc_bf16(true);
+      mbar_wait(bar_q, 0);
+      tc_fence_after();
+      int slot = 0;
+      uint32_t phase = 0;
+      auto issue_s = [&](int j) {
+        const int b = j & 1;
+        if (j >= 2) mbar_wait(bar_sempty(b), ((j >> 1) - 1) & 1);
+        mbar_wait(bar_full(slot), phase);
+        tc_fence_after();
+        const uint32_t k_tile = sKV + slot * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
+          tc_mma(tS[b], sdesc(sQ + off, 16, 1024), sdesc(k_tile + off, 16, 1024), IDESC_S,
+                 kk > 0);
+        }
+        tc_commit(bar_empty(slot));
+        tc_commit(bar_sfull(b));
+        if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
+      };
+      issue_s(0);
+      for (int j = 0; j < nb; ++j) {
+        if (j + 1 < nb) issue_s(j + 1);
+        // O += P_j V_j
+        const int b = j & 1;
+        mbar_wait(bar_pfull(b), (j >> 1) & 1);
+        mbar_wait(bar_full(slot), phase);
+        tc_fence_after();
+        const uint32_t v_tile = sKV + slot * TILE_BYTES;
+        const uint32_t p_tile = sP + b * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BLK_N / 16; ++kk) {
+          const uint32_t aoff = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
+          // V: MN-major, K-step of 16 keys = 2 x 1024 B core-matrix groups
+          tc_mma(tO, sdesc(p_tile + aoff, 16, 1024), sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024),
+                 IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc_commit(bar_empty(slot));
+        tc_commit(bar_pempty(b));
+        tc_commit(bar_odone);
+        if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax (rows)
+    const int m = threadIdx.x;  // TMEM lane / tile row
+    const int qi = m / p.G, hj = m % p.G;
+    const int a = a0 + qi;
+    const bool valid = a < p.A;
+    const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    uint32_t r[BLK_N];
+    for (int j = 0; j < nb; ++j) {
+      const int b = j & 1;
+      mbar_wait(bar_sfull(b), (j >> 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BLK_N / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, r + c * 32);
+#pragma unroll
+      for (int c = 0; c < BLK_N / 32; ++c) tmem_wait_ld32(r + c * 32);
+      tc_fence_before();
+      mbar_arrive(bar_sempty(b));
+      const int kbase = j * BLK_N;
+      float mx = -INFINITY;
+      const bool need_mask = kbase + BLK_N - 1 > pos;
+#pragma unroll
+      for (int c = 0; c < BLK_N; ++c) {
+        float s = __uint_as_float(r[c]) * p.scale_log2;
+        if (need_mask && kbase + c > pos) s = -INFINITY;
+        r[c] = __float_as_uint(s);
+        mx = fmaxf(mx, s);
+      }
+      const float m_new = fmaxf(m_used, mx);
+      const bool grow = m_new > m_used + LAZY_THRESH;
+      // warp-uniform decision: tcgen05.ld/st are .sync.aligned
+      if (__any_sync(0xffffffffu, grow)) {
+        const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
+        if (j > 0) {
+          // rescale O in TMEM once PV_{j-1} has landed
+          mbar_wait(bar_odone, (j - 1) & 1);
+          tc_fence_after();
+#pragma unroll 1
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO + lane_off + c * 32, o);
+            tmem_wait_ld32(o);
+#pragma unroll
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st32(tO + lane_off + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+        l *= corr;
+        if (grow) m_used = m_new;
+      }
+      float sum = 0.f;
+      // P_j into smem buffer b (K-major SW128: row m, 16-B chunk c^(m&7))
+      if (j >= 2) mbar_wait(bar_pempty(b), ((j >> 1) - 1) & 1);
+      uint8_t* prow = gP + b * TILE_BYTES + m * 128;
+#pragma unroll
+      for (int ch = 0; ch < BLK_N / 8; ++ch) {
+        float e[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) {
+          e[t] = ex2(__uint_as_float(r[ch * 8 + t]) - m_used);
+          sum += e[t];
+        }
+        uint4 v;
+        v.x = pack_bf16(e[0], e[1]);
+        v.y = pack_bf16(e[2], e[3]);
+        v.z = pack_bf16(e[4], e[5]);
+        v.w = pack_bf16(e[6], e[7]);
+        const int atom = ch >> 3, c8 = ch & 7;
+        *reinterpret_cast<uint4*>(prow + atom * ATOM_BYTES + ((c8 ^ (m & 7)) << 4)) = v;
+      }
+      l += sum;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      tc_fence_before();
+      mbar_arrive(bar_pfull(b));
+    }
+    // epilogue: O / l -> global
+    mbar_wait(bar_odone, (nb - 1) & 1);
+    tc_fence_after();
+    const float inv = valid ? 1.f / l : 0.f;
+    const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tO + lane_off + c * 32, o);
+      tmem_wait_ld32(o);
+      if (valid) {
+        if (p.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(p.out_f32 + orow + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
+            dst[e] = v;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                 : "memory");
+  }
+}
+
+using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = (EncodeFn)p;
+  }
+  return fn;
+}
+
+static int make_map(CUtensorMap* map, const void* ptr, uint64_t d1, uint64_t d2,
+                    uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1, uint32_t box2) {
+  EncodeFn enc = encode_fn();
+  if (!enc) return fail(CT_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[3] = {HD, d1, d2};
+  cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+  cuuint32_t box[3] = {64, box1, box2};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides,
+                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(CT_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return CT_OK;
+}
+
+}  // namespace tc
+
+bool tc_enabled() { return true; }
+
+size_t attention_tc_workspace(int64_t, int64_t, int64_t, int64_t, int64_t) { return 0; }
+
+int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, const void* k_cache,
+                 const void* v_cache, int64_t n_ctx, int64_t Hkv, int64_t D,
+                 int64_t cache_row_stride, double scale, void* out, int out_dtype,
+                 void* workspace, size_t workspace_bytes, cudaStream_t st) {
+  using namespace tc;
+  (void)workspace;
+  (void)workspace_bytes;
+  if (D != HD) return fail(CT_ERR_UNSUPPORTED, "tcgen05 attention needs head_dim 128");
+  const int64_t G = Hq / Hkv;
+  if (G < 1 || TILE_M % G) return fail(CT_ERR_UNSUPPORTED, "GQA group %lld must divide 128", (long long)G);
+  if (((uintptr_t)q | (uintptr_t)k_cache | (uintptr_t)v_cache) & 15)
+    return fail(CT_ERR_PARAM, "tensors must be 16-byte aligned");
+  if ((cache_row_stride * 2) % 16) return fail(CT_ERR_PARAM, "cache row stride alignment");
+  CUtensorMap mq, mk, mv;
+  int rc;
+  if ((rc = make_map(&mq, q, (uint64_t)Hq, (uint64_t)A, HD * 2, (uint64_t)Hq * HD * 2,
+                     (uint32_t)G, (uint32_t)(TILE_M / G))))
+    return rc;
+  if ((rc = make_map(&mk, k_cache, (uint64_t)Hkv, (uint64_t)n_ctx, HD * 2,
+                     (uint64_t)cache_row_stride * 2, 1, BLK_N)))
+    return rc;
+  if ((rc = make_map(&mv, v_cache, (uint64_t)Hkv, (uint64_t)n_ctx, HD * 2,
+                     (uint64_t)cache_row_stride * 2, 1, BLK_N)))
+    return rc;
+  Params prm;
+  prm.qpos = q_pos;
+  prm.out = out_dtype == CT_BF16 ? (__nv_bfloat16*)out : nullptr;
+  prm.out_f32 = out_dtype == CT_F32 ? (float*)out : nullptr;
+  prm.A = (int)A;
+  prm.Hq = (int)Hq;
+  prm.Hkv = (int)Hkv;
+  prm.G = (int)G;
+  prm.QB = (int)(TILE_M / G);
+  prm.n_ctx = (int)n_ctx;
+  prm.n_qblocks = (int)((A + prm.QB - 1) / prm.QB);
+  prm.scale_log2 = (float)(scale * 1.4426950408889634);
+  const size_t smem = Smem::TOTAL + 1024;
+  CT_CUDA(cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  const unsigned grid = (unsigned)(prm.n_qblocks * Hkv);
+  attention_tc_kernel<<<grid, THREADS, smem, st>>>(mq, mk, mv, prm);
+  return check_launch("attention_tc_kernel");
+}
+
 }  // namespace ct

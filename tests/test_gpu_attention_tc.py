@@ -1,0 +1,83 @@
+"""tcgen05/TMEM attention kernel (bf16 operands, fp32 accumulation) against a
+plain PyTorch fp32 reference of ct/toymodel.py:176-183 on the same bf16
+inputs.  Tolerance: normwise 1e-2 (bf16 P rounding), per-row checks for the
+masking edge cases."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _ref(q, pos, k, v, hq, hkv):
+    a, _, d = q.shape
+    n = k.shape[0]
+    g = hq // hkv
+    kk = k.float().repeat_interleave(g, dim=1).permute(1, 2, 0)
+    vv = v.float().repeat_interleave(g, dim=1).permute(1, 0, 2)
+    s = torch.bmm(q.float().permute(1, 0, 2), kk) / d ** 0.5
+    mask = torch.arange(n, device=q.device)[None, :] <= pos[:, None].long()
+    s = s.masked_fill(~mask[None], float("-inf"))
+    return torch.bmm(torch.softmax(s, dim=-1), vv).permute(1, 0, 2)
+
+
+def _run(q, pos, k, v, hq, hkv, out_dtype=torch.bfloat16):
+    from paper_2605_24022_b200 import _dev, _lib
+    a, _, d = q.shape
+    n = k.shape[0]
+    out = torch.empty((a, hq, d), device="cuda", dtype=out_dtype)
+    _lib.call("ct_selective_attention", _dev.ptr(q), _dev.ptr(pos), a, hq, _dev.ptr(k),
+              _dev.ptr(v), n, hkv, d, k.stride(0), 1.0 / d ** 0.5, _lib.CT_BF16, _dev.ptr(out),
+              _dev.ct_dtype(out_dtype), None, None, 0, _dev.stream_handle())
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("a,hq,hkv,n,sorted_pos", [
+    (32, 32, 8, 128, True),       # one tile, one key block
+    (300, 32, 8, 2500, True),     # ragged tail, GQA 4
+    (1000, 8, 8, 5000, True),     # MHA (G=1), 8 q-blocks
+    (77, 16, 2, 3001, False),     # G=8, unsorted positions
+    (4992, 32, 8, 32832, True),   # config-2 layer shape (selected + suffix rows)
+])
+def test_tc_attention_matches_torch(a, hq, hkv, n, sorted_pos):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    gen = torch.Generator(device="cuda").manual_seed(a + n)
+    d = 128
+    q = torch.randn((a, hq, d), device="cuda", generator=gen).to(torch.bfloat16)
+    k = torch.randn((n, hkv, d), device="cuda", generator=gen).to(torch.bfloat16)
+    v = torch.randn((n, hkv, d), device="cuda", generator=gen).to(torch.bfloat16)
+    pos = torch.randperm(n, device="cuda", generator=gen)[:a]
+    if sorted_pos:
+        pos = torch.sort(pos)[0]
+    pos = pos.to(torch.int32)
+    pos[0] = 0 if sorted_pos else pos[0]
+    out = _run(q, pos, k, v, hq, hkv)
+    if a * hq * n > 2e9:   # keep the torch reference affordable: sample query rows
+        idx = torch.randperm(a, device="cuda", generator=gen)[:256]
+        want = _ref(q[idx], pos[idx], k, v, hq, hkv)
+        got = out[idx].float()
+    else:
+        want = _ref(q, pos, k, v, hq, hkv)
+        got = out.float()
+    err = (got - want).abs().max().item() / want.abs().max().item()
+    assert err < 1e-2, err
+
+
+def test_tc_attention_f32_output_and_large_scores():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    a, hq, hkv, n, d = 200, 8, 2, 1500, 128
+    # large logits exercise the lazy-rescale path (max grows by > 2^8 mid-row)
+    q = (4 * torch.randn((a, hq, d), device="cuda", generator=gen)).to(torch.bfloat16)
+    k = torch.randn((n, hkv, d), device="cuda", generator=gen)
+    k[700:] *= 3
+    k = k.to(torch.bfloat16)
+    v = torch.randn((n, hkv, d), device="cuda", generator=gen).to(torch.bfloat16)
+    pos = torch.sort(torch.randperm(n, device="cuda", generator=gen)[:a])[0].to(torch.int32)
+    out = _run(q, pos, k, v, hq, hkv, out_dtype=torch.float32)
+    want = _ref(q, pos, k, v, hq, hkv)
+    err = (out - want).abs().max().item() / want.abs().max().item()
+    assert err < 1e-2, err
