@@ -127,7 +127,14 @@ def last_error() -> str:
     return buf.value.decode(errors="replace")
 
 
+# kernel-launching entry points seen through check()/call() (bench evidence)
+LAUNCH_COUNT = {"n": 0}
+_NOT_KERNELS = {"ct_copy_ranges_h2d", "ct_host_alloc", "ct_host_free"}
+
+
 def check(status: int, what: str = "") -> None:
+    if what not in _NOT_KERNELS:
+        LAUNCH_COUNT["n"] += 1
     if status != 0:
         cls = _STATUS.get(status, CacheTuneError)
         raise cls(f"{what}: {last_error()}" if what else last_error())

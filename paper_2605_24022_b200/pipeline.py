@@ -1,0 +1,209 @@
+"""Serving-shaped engines for repeated requests over a resident chunk pool.
+
+`SelectivePrefillEngine` is the online path of ct/toymodel.py:223-311 with
+every buffer preallocated, the selection plan, the sparse transfer and the
+deferred-RoPE blend wired to a `KvPool`:
+
+  * pool in HBM ("hbm"): K3 reads each (chunk, layer) keep tail in place.
+  * pool in pinned host memory ("pinned"): all (chunk, layer) tails are issued
+    up front as ONE cudaMemcpyAsync each on a copy stream (copy engines, no SM
+    time); layer l's blend waits only on layer l's copy event, so PCIe runs
+    flat out underneath the per-layer recompute (the three-stream overlap of
+    ct/pipesim.py:196-241, collection layer = layer 0's transfer).
+
+`FullPrefillEngine` is the full-recompute baseline built from the same
+kernels (every token a query, dense causal).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .model import GpuModel
+from .pool import KvPool
+from .prefill import NORM_EPS, LayerBuffers, run_layers  # noqa: F401
+from .rope import rope_table
+from .spectral import selection_count
+
+
+class KernelTimer:
+    """CUDA-event pairs around named launches on the current stream."""
+
+    def __init__(self):
+        self.enabled = False
+        self.events: dict = {}
+
+    def start(self, name):
+        if not self.enabled:
+            return None
+        s = torch.cuda.Event(enable_timing=True)
+        s.record()
+        return s
+
+    def stop(self, name, s):
+        if s is None:
+            return
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.events.setdefault(name, []).append((s, e))
+
+    def mean_ms(self, name) -> float:
+        ev = self.events.get(name, [])
+        if not ev:
+            return float("nan")
+        return float(np.mean([s.elapsed_time(e) for s, e in ev]))
+
+    def count(self, name) -> int:
+        return len(self.events.get(name, []))
+
+    def reset(self):
+        self.events = {}
+
+
+class SelectivePrefillEngine:
+    def __init__(self, model: GpuModel, pool: KvPool, r: float, suffix_len: int,
+                 timer: KernelTimer | None = None):
+        cfg = model.config
+        if (pool.L, pool.H, pool.D) != (cfg.n_layers, cfg.kv_heads, cfg.head_dim):
+            raise ValueError("pool geometry disagrees with model")
+        self.model, self.pool, self.r, self.S = model, pool, r, suffix_len
+        self.timer = timer or KernelTimer()
+        dev = model.device
+        C, N, L, H, D = pool.C, pool.N, pool.L, pool.H, pool.D
+        self.k = selection_count(r, N)
+        self.n_keep = N - self.k
+        self.history = C * N
+        self.n_ctx = self.history + suffix_len
+        self.n_rec = C * self.k
+        self.A = self.n_rec + suffix_len
+        dt = model.dtype
+        self.cache = torch.empty((L, 2, self.n_ctx, H, D), dtype=dt, device=dev)
+        self.caches = [(self.cache[l, 0], self.cache[l, 1]) for l in range(L)]
+        self.buffers = LayerBuffers(model, self.A, dev)
+        self.positions = torch.empty(self.A, dtype=torch.int32, device=dev)
+        self.tokens = torch.empty(self.A, dtype=torch.int32, device=dev)
+        self.positions[self.n_rec:] = torch.arange(self.history, self.n_ctx, dtype=torch.int32,
+                                                   device=dev)
+        self.keep = torch.empty(C * self.n_keep, dtype=torch.int32, device=dev)
+        self.keep_src = torch.empty_like(self.keep)
+        offsets = np.arange(C + 1, dtype=np.int64) * N
+        meta = np.concatenate([offsets, np.full(C, self.k), np.arange(C + 1) * self.k,
+                               np.arange(C + 1) * self.n_keep]).astype(np.int64)
+        self.meta = torch.as_tensor(meta, device=dev)
+        self.table = rope_table(cfg.rope_params, self.n_ctx, "f64" if dt == torch.float32
+                                else "f32", dev)
+        self.pinned = pool.location == "pinned"
+        row = pool.row_bytes
+        self.row_elems = H * D
+        if self.pinned:
+            self.stage = torch.empty((L, C, max(self.n_keep, 1), 2, H, D), dtype=dt, device=dev)
+            self.copy_stream = torch.cuda.Stream(device=dev)
+            self.copy_done = [torch.cuda.Event() for _ in range(L)]
+            self.step_start = torch.cuda.Event()
+            nbytes = self.n_keep * 2 * row
+            self.copy_args = []
+            for l in range(L):
+                dst = [self.stage[l, c].data_ptr() for c in range(C)]
+                src = [pool.tail_ptr(c, l, self.k) for c in range(C)]
+                self.copy_args.append(((ctypes.c_void_p * C)(*dst), (ctypes.c_void_p * C)(*src),
+                                       (ctypes.c_int64 * C)(*([nbytes] * C))))
+            self.h2d_bytes = L * C * nbytes
+        else:
+            self.h2d_bytes = 0
+        # per-layer K3 segments (kernel parameters, built once)
+        esz = pool.esize
+        self.segs = []
+        for l in range(L):
+            segs = []
+            for c in range(C):
+                if self.n_keep == 0:
+                    continue
+                base = self.stage[l, c].data_ptr() if self.pinned else pool.tail_ptr(c, l, self.k)
+                tok = pool.agg.data_ptr() + (c * N + self.k) * 4
+                segs.append(_lib.Segment(base, base + H * D * esz, tok, self.n_keep, c * N, 0))
+            self.segs.append((_lib.Segment * max(len(segs), 1))(*segs) if segs else None)
+        self.n_segs = C if self.n_keep else 0
+        self.launches_per_step = None
+
+    # algorithmic work per request -------------------------------------------------
+    def attention_flops_per_layer(self) -> float:
+        pos = self.positions.double().cpu().numpy()
+        cfg = self.model.config
+        return float(4.0 * cfg.n_heads * cfg.head_dim * np.sum(pos + 1.0))
+
+    def blend_bytes_per_layer(self) -> int:
+        # read keep rows (K and V) + write them into the cache
+        return 2 * 2 * self.pool.C * self.n_keep * self.pool.row_bytes
+
+    def _reuse(self, l: int) -> None:
+        if self.n_segs == 0:
+            return
+        st = _dev.stream_handle()
+        if self.pinned:
+            torch.cuda.current_stream().wait_event(self.copy_done[l])
+        t = self.timer.start("blend")
+        pool = self.pool
+        _lib.call("ct_gather_rope_blend", self.segs[l], self.n_segs, 2 * self.row_elems,
+                  pool.H, pool.D, _dev.ct_dtype(pool.dtype),
+                  self.model.config.rope_params.pairing_code, _dev.ptr(self.table),
+                  _dev.ptr(self.cache[l, 0]), _dev.ptr(self.cache[l, 1]), self.row_elems, st)
+        self.timer.stop("blend", t)
+
+    def step(self, suffix=None, logits_out: torch.Tensor | None = None) -> torch.Tensor:
+        """One request: suffix (host pinned or device int32 [S]) -> last-row logits."""
+        pool, st = self.pool, _dev.stream_handle()
+        C, N = pool.C, pool.N
+        if self.pinned:
+            self.step_start.record()
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_event(self.step_start)
+                cs = _dev.stream_handle(self.copy_stream)
+                for l in range(pool.L):
+                    d, s, b = self.copy_args[l]
+                    _lib.call("ct_copy_ranges_h2d", d, s, b, C, cs)
+                    self.copy_done[l].record(self.copy_stream)
+        if suffix is not None and self.S:
+            self.tokens[self.n_rec:].copy_(suffix, non_blocking=True)
+        m = self.meta
+        _lib.call("ct_selection_plan", _dev.ptr(pool.agg), _dev.ptr(m[:C + 1]),
+                  _dev.ptr(m[C + 1:2 * C + 1]), _dev.ptr(m[2 * C + 1:3 * C + 2]),
+                  _dev.ptr(m[3 * C + 2:]), C, N, _dev.ptr(self.positions), _dev.ptr(self.keep),
+                  _dev.ptr(self.keep_src), st)
+        if self.n_rec:
+            _lib.call("ct_gather_rows", _dev.ptr(pool.tokens), _dev.ptr(self.positions),
+                      self.n_rec, 4, _dev.ptr(self.tokens), st)
+        logits, _ = run_layers(self.model, self.tokens, self.positions, self.n_ctx, self.caches,
+                               reuse=self._reuse, logits_rows="last", buffers=self.buffers,
+                               timer=self.timer)
+        if logits_out is not None:
+            logits_out.copy_(logits, non_blocking=True)
+        return logits
+
+
+class FullPrefillEngine:
+    """Full-recompute baseline (ct/toymodel.py:196-205) with the same kernels."""
+
+    def __init__(self, model: GpuModel, n_ctx: int, timer: KernelTimer | None = None):
+        cfg = model.config
+        dev = model.device
+        self.model, self.n_ctx = model, n_ctx
+        self.timer = timer or KernelTimer()
+        self.cache = torch.empty((cfg.n_layers, 2, n_ctx, cfg.kv_heads, cfg.head_dim),
+                                 dtype=model.dtype, device=dev)
+        self.caches = [(self.cache[l, 0], self.cache[l, 1]) for l in range(cfg.n_layers)]
+        self.buffers = LayerBuffers(model, n_ctx, dev)
+        self.positions = torch.arange(n_ctx, dtype=torch.int32, device=dev)
+
+    def attention_flops_per_layer(self) -> float:
+        cfg = self.model.config
+        n = self.n_ctx
+        return 4.0 * cfg.n_heads * cfg.head_dim * n * (n + 1) / 2.0
+
+    def step(self, tokens: torch.Tensor) -> torch.Tensor:
+        logits, _ = run_layers(self.model, tokens, self.positions, self.n_ctx, self.caches,
+                               logits_rows="last", buffers=self.buffers, timer=self.timer)
+        return logits

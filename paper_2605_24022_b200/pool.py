@@ -1,0 +1,169 @@
+"""(2) Importance-ordered KV pool and sparse transfer.
+
+The reference stores each chunk token-major in a CTKV file and fetches the
+keep set (complement of the recompute set) as coalesced byte ranges --
+~400 ranges per (chunk, layer) at config-2 size (ct/cachepool.py:409-481,
+SURVEY F8).  Here each chunk's rows are stored in its AGGREGATE IMPORTANCE
+ORDER (ct/spectral.py:149-159), K row then V row, layer-major:
+
+    data[c, l, p, 0|1, H, D] = K|V of token aggregate_order[c][p] at layer l
+
+so for any ratio r the keep set of (c, l) is the contiguous tail
+p in [ceil(rN), N): ONE copy-engine transfer per (chunk, layer), and the
+deferred-RoPE blend kernel reads it with the permutation aggregate_order[k:].
+The pool lives in HBM (`location="hbm"`) or pinned host memory
+(`location="pinned"`, copied by the copy engines on a side stream).
+Byte accounting matches the reference: bytes moved per (chunk, layer) =
+|keep| * H * D * dsize * 2 (ct/cachepool.py:434).
+"""
+
+from __future__ import annotations
+
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .errors import InvalidParam, InvalidPlan, NotFound
+from .spectral import ImportanceRanking, selection_count
+
+
+@dataclass(frozen=True)
+class SparseFetchPlan:
+    """Byte-exact plan for one (chunk, layer) at ratio r (ct/cachepool.py:236-255).
+
+    byte_ranges are (offset, length) into the pool's flat byte image; with the
+    importance-ordered layout there is exactly one range (or none)."""
+    chunk_id: str
+    layer: int
+    keep_indices: np.ndarray
+    byte_ranges: tuple
+    expected_bytes: int
+    keep_count: int
+
+
+class KvPool:
+    """Importance-ordered pool of equal-geometry chunks."""
+
+    def __init__(self, chunks, rankings, location: str = "hbm", device=None):
+        if len(chunks) == 0 or len(chunks) != len(rankings):
+            raise InvalidPlan("need one ranking per chunk")
+        if location not in ("hbm", "pinned"):
+            raise InvalidParam(f"unknown pool location {location!r}")
+        device = device or _dev.require_cuda()
+        c0 = chunks[0]
+        L, N, H, D = c0.keys.shape
+        for c, rk in zip(chunks, rankings):
+            if tuple(c.keys.shape) != (L, N, H, D):
+                raise InvalidParam("pool chunks must share one geometry")
+            if rk.n_tokens != N:
+                raise InvalidPlan("ranking/chunk token counts disagree")
+        self.location = location
+        self.device = torch.device(device)
+        self.dtype = c0.keys.dtype
+        self.C, self.L, self.N, self.H, self.D = len(chunks), L, N, H, D
+        self.chunk_ids = [c.chunk_id for c in chunks]
+        self.rankings = list(rankings)
+        self.esize = torch.empty((), dtype=self.dtype).element_size()
+        self.row_bytes = H * D * self.esize
+        self.agg = torch.stack([rk.aggregate_device(self.device) for rk in rankings]).contiguous()
+        self.tokens = torch.stack([
+            c.tokens if c.tokens is not None else
+            torch.as_tensor(np.asarray(c.source_tokens, np.int32), device=self.device)
+            for c in chunks]).contiguous()
+        self.tokens_host = np.stack([np.asarray(c.source_tokens, np.int64) for c in chunks])
+        shape = (self.C, L, N, 2, H, D)
+        dev_img = torch.empty(shape, dtype=self.dtype, device=self.device)
+        tmp = torch.empty((N, H, D), dtype=self.dtype, device=self.device)
+        for ci, c in enumerate(chunks):   # offline: permute rows into importance order
+            perm = self.agg[ci]
+            for l in range(L):
+                for side, src in ((0, c.keys[l]), (1, c.values[l])):
+                    _lib.call("ct_gather_rows", _dev.ptr(src), _dev.ptr(perm), N,
+                              self.row_bytes, _dev.ptr(tmp), _dev.stream_handle())
+                    dev_img[ci, l, :, side].copy_(tmp)
+        if location == "hbm":
+            self.data = dev_img
+        else:
+            self.data = torch.empty(shape, dtype=self.dtype, pin_memory=True)
+            self.data.copy_(dev_img)
+            del dev_img
+        self._stats_lock = threading.Lock()
+        self.io_stats = {"bytes_read": 0, "reads": 0}
+
+    # -- geometry ----------------------------------------------------------
+    @property
+    def nbytes(self) -> int:
+        return self.data.numel() * self.esize
+
+    def chunk_index(self, chunk_id) -> int:
+        if isinstance(chunk_id, int):
+            return chunk_id
+        try:
+            return self.chunk_ids.index(chunk_id)
+        except ValueError:
+            raise NotFound(f"chunk {chunk_id!r} not in pool") from None
+
+    def offset_bytes(self, c: int, l: int, p: int) -> int:
+        return (((c * self.L + l) * self.N + p) * 2) * self.row_bytes
+
+    def tail_ptr(self, c: int, l: int, k: int) -> int:
+        return self.data.data_ptr() + self.offset_bytes(c, l, k)
+
+    # -- reference-shaped sparse API (ct/cachepool.py:409-481) ------------------
+    def plan_sparse_fetch(self, chunk_id, layer: int, r: float) -> SparseFetchPlan:
+        c = self.chunk_index(chunk_id)
+        if not 0 <= layer < self.L:
+            raise InvalidParam(f"layer {layer} out of range [0, {self.L})")
+        k = selection_count(r, self.N)
+        keep = np.sort(self.rankings[c].aggregate_order[k:])
+        n_keep = self.N - k
+        length = n_keep * 2 * self.row_bytes
+        ranges = ((self.offset_bytes(c, layer, k), length),) if n_keep else ()
+        return SparseFetchPlan(self.chunk_ids[c], layer, keep, ranges, n_keep * self.row_bytes * 2,
+                               n_keep)
+
+    def fetch_sparse(self, plan: SparseFetchPlan, stream=None):
+        """Move exactly the planned bytes to HBM; return (K [keep,H,D], V, keep)
+        in ascending token order like the reference."""
+        c = self.chunk_index(plan.chunk_id)
+        if plan.expected_bytes != len(plan.keep_indices) * self.row_bytes * 2:
+            raise InvalidPlan("expected_bytes disagrees with keep_indices")
+        n_keep = plan.keep_count
+        if n_keep == 0:
+            return None, None, plan.keep_indices
+        k = self.N - n_keep
+        stage = torch.empty((n_keep, 2, self.H, self.D), dtype=self.dtype, device=self.device)
+        src = self.tail_ptr(c, plan.layer, k)
+        nbytes = plan.byte_ranges[0][1]
+        dst = (ctypes_ptr_array([stage.data_ptr()]), ctypes_ptr_array([src]),
+               ctypes_i64_array([nbytes]))
+        if self.location == "pinned":
+            _lib.call("ct_copy_ranges_h2d", dst[0], dst[1], dst[2], 1, _dev.stream_handle(stream))
+        else:
+            stage.view(-1).view(torch.uint8).copy_(
+                self.data.view(-1)[self.offset_bytes(c, plan.layer, k) // self.esize:
+                                   self.offset_bytes(c, plan.layer, k) // self.esize
+                                   + nbytes // self.esize].view(torch.uint8))
+        with self._stats_lock:
+            self.io_stats["bytes_read"] += nbytes
+            self.io_stats["reads"] += 1
+        # un-permute: output row i = token keep[i] = tail row rank[keep[i]] - k
+        rank = np.argsort(self.rankings[c].aggregate_order)
+        rows = torch.as_tensor((rank[plan.keep_indices] - k).astype(np.int32), device=self.device)
+        kv = torch.empty_like(stage)
+        _lib.call("ct_gather_rows", _dev.ptr(stage), _dev.ptr(rows), n_keep, 2 * self.row_bytes,
+                  _dev.ptr(kv), _dev.stream_handle(stream))
+        return kv[:, 0], kv[:, 1], plan.keep_indices
+
+
+def ctypes_ptr_array(vals):
+    import ctypes
+    return (ctypes.c_void_p * len(vals))(*vals)
+
+
+def ctypes_i64_array(vals):
+    import ctypes
+    return (ctypes.c_int64 * len(vals))(*vals)

@@ -128,7 +128,8 @@ def _mm_f32(a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
 def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n_ctx: int,
                caches: Sequence, reuse: Callable[[int], None] | None = None,
                record_attention: bool = False, logits_rows: str | None = "all",
-               k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None):
+               k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None,
+               timer=None):
     """Shared forward engine (ct/toymodel.py:135-193) over device inputs.
 
     tokens/positions: int32 [A] device.  caches[l] = (K, V) [n_ctx, Hkv, D]
@@ -165,10 +166,13 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
             reuse(l)
         probs = (torch.empty((hq, a, n_ctx), dtype=torch.float32, device=dev)
                  if record_attention else None)
+        t0 = timer.start("attention") if timer is not None else None
         _lib.check(lib.ct_selective_attention(
             _dev.ptr(buf.q), _dev.ptr(positions), a, hq, _dev.ptr(kc), _dev.ptr(vc), n_ctx, hkv,
-            d, hkv * d, scale, dtc, _dev.ptr(buf.ctx), dtc, _dev.ptr(probs), _dev.ptr(ws), wsb,
-            st), "ct_selective_attention")
+            d, kc.stride(0), scale, dtc, _dev.ptr(buf.ctx), dtc, _dev.ptr(probs), _dev.ptr(ws),
+            wsb, st), "ct_selective_attention")
+        if timer is not None:
+            timer.stop("attention", t0)
         if record_attention:
             probs_all.append(probs)
         o = _mm_f32(buf.ctx, w["wo"])
