@@ -160,6 +160,50 @@ __device__ __forceinline__ float ex2(float x) {
   return y;
 }
 
+// --- packed fp32 (FFMA2 / FADD2) and 3-input max helpers (sm_100a) ----------
+__device__ __forceinline__ uint64_t pk2(float a, float b) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ uint64_t ffma2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t fadd2(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ float max3f(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// 2^x for x <= ~8 on the FMA pipe: round-to-nearest split x = n + f, f in
+// [-1/2, 1/2], degree-3 minimax 2^f (max rel err 7.5e-5, below bf16 P
+// rounding), exponent add.  x clamped at -126 (result ~1e-38, i.e. zero).
+__device__ __forceinline__ void exp2_poly2(uint64_t x2, uint32_t& o0, uint32_t& o1) {
+  float a, b;
+  upk2(x2, a, b);
+  const uint64_t xc = pk2(fmaxf(a, -126.f), fmaxf(b, -126.f));
+  const uint64_t t = fadd2(xc, pk2(12582912.f, 12582912.f));
+  const uint64_t rr = fadd2(t, pk2(-12582912.f, -12582912.f));
+  const uint64_t f = ffma2(rr, pk2(-1.f, -1.f), xc);
+  uint64_t pp = ffma2(f, pk2(0.05517025291919708f, 0.05517025291919708f),
+                      pk2(0.24260790646076202f, 0.24260790646076202f));
+  pp = ffma2(pp, f, pk2(0.693260908126831f, 0.693260908126831f));
+  pp = ffma2(pp, f, pk2(0.9999282956123352f, 0.9999282956123352f));
+  o0 = (uint32_t)pp + ((uint32_t)t << 23);
+  o1 = (uint32_t)(pp >> 32) + ((uint32_t)(t >> 32) << 23);
+}
+// 16 chunks of 8 scores per block; these 6 use the polynomial (~37%).
+constexpr uint32_t POLY_MASK = (1u << 1) | (1u << 4) | (1u << 7) | (1u << 9) | (1u << 12) | (1u << 15);
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -173,6 +217,8 @@ struct Params {
   int n_ctx;
   int n_qblocks;
   float scale_log2;
+  float lazy_thresh;
+  uint32_t poly_mask;
 };
 
 __global__ void __launch_bounds__(THREADS, 1)
@@ -308,7 +354,6 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         }
         tc_commit(bar_empty(slot));
         tc_commit(bar_pempty(b));
-        tc_commit(bar_odone);
         if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
       }
     }
@@ -333,23 +378,32 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       tc_fence_before();
       mbar_arrive(bar_sempty(b));
       const int kbase = j * BLK_N;
-      float mx = -INFINITY;
       const bool need_mask = kbase + BLK_N - 1 > pos;
+      if (need_mask) {
 #pragma unroll
-      for (int c = 0; c < BLK_N; ++c) {
-        float s = __uint_as_float(r[c]) * p.scale_log2;
-        if (need_mask && kbase + c > pos) s = -INFINITY;
-        r[c] = __float_as_uint(s);
-        mx = fmaxf(mx, s);
+        for (int c = 0; c < BLK_N; ++c)
+          if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
       }
+      // row max of the raw scores (scale > 0 commutes with max): 4 FMNMX3 chains
+      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < BLK_N; c += 8) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
+      }
+      const float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
-      const bool grow = m_new > m_used + LAZY_THRESH;
+      const bool grow = m_new > m_used + p.lazy_thresh;
       // warp-uniform decision: tcgen05.ld/st are .sync.aligned
       if (__any_sync(0xffffffffu, grow)) {
         const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
         if (j > 0) {
           // rescale O in TMEM once PV_{j-1} has landed
-          mbar_wait(bar_odone, (j - 1) & 1);
+          // PV_{j-1} done.  Wait on its P-buffer barrier: this thread already
+          // waited that barrier's previous phase (PV_{j-3}), so the parity test
+          // cannot alias (a shared "O done" barrier could be 2 phases behind).
+          mbar_wait(bar_pempty((j - 1) & 1), ((j - 1) >> 1) & 1);
           tc_fence_after();
 #pragma unroll 1
           for (int c = 0; c < HD / 32; ++c) {
@@ -365,33 +419,57 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         l *= corr;
         if (grow) m_used = m_new;
       }
-      float sum = 0.f;
-      // P_j into smem buffer b (K-major SW128: row m, 16-B chunk c^(m&7))
+      // P_j into smem buffer b (K-major SW128: row m, 16-B chunk c^(m&7)).
+      // x = s*scale - m (FFMA2); 2^x on MUFU for most chunks and on the FMA
+      // pipe (degree-3 polynomial) for POLY_MASK chunks to balance the pipes.
       if (j >= 2) mbar_wait(bar_pempty(b), ((j >> 1) - 1) & 1);
       uint8_t* prow = gP + b * TILE_BYTES + m * 128;
+      const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
+      const uint64_t nm2 = pk2(-m_used, -m_used);
+      uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
 #pragma unroll
       for (int ch = 0; ch < BLK_N / 8; ++ch) {
-        float e[8];
+        uint64_t x2[4];
 #pragma unroll
-        for (int t = 0; t < 8; ++t) {
-          e[t] = ex2(__uint_as_float(r[ch * 8 + t]) - m_used);
-          sum += e[t];
+        for (int t = 0; t < 4; ++t)
+          x2[t] = ffma2(pk2(__uint_as_float(r[ch * 8 + 2 * t]), __uint_as_float(r[ch * 8 + 2 * t + 1])),
+                        sc2, nm2);
+        uint32_t e[8];
+        if (((p.poly_mask >> ch) & 1) && !need_mask) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) exp2_poly2(x2[t], e[2 * t], e[2 * t + 1]);
+        } else {
+#pragma unroll
+          for (int t = 0; t < 4; ++t) {
+            float a, bb;
+            upk2(x2[t], a, bb);
+            e[2 * t] = __float_as_uint(ex2(a));
+            e[2 * t + 1] = __float_as_uint(ex2(bb));
+          }
         }
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e[2 * t] | ((uint64_t)e[2 * t + 1] << 32));
         uint4 v;
-        v.x = pack_bf16(e[0], e[1]);
-        v.y = pack_bf16(e[2], e[3]);
-        v.z = pack_bf16(e[4], e[5]);
-        v.w = pack_bf16(e[6], e[7]);
+        v.x = pack_bf16(__uint_as_float(e[0]), __uint_as_float(e[1]));
+        v.y = pack_bf16(__uint_as_float(e[2]), __uint_as_float(e[3]));
+        v.z = pack_bf16(__uint_as_float(e[4]), __uint_as_float(e[5]));
+        v.w = pack_bf16(__uint_as_float(e[6]), __uint_as_float(e[7]));
         const int atom = ch >> 3, c8 = ch & 7;
         *reinterpret_cast<uint4*>(prow + atom * ATOM_BYTES + ((c8 ^ (m & 7)) << 4)) = v;
       }
-      l += sum;
+      {
+        float s0, s1, s2, s3;
+        upk2(acc2[0], s0, s1);
+        upk2(acc2[1], s2, s3);
+        l += (s0 + s1) + (s2 + s3);
+      }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       tc_fence_before();
       mbar_arrive(bar_pfull(b));
     }
     // epilogue: O / l -> global
-    mbar_wait(bar_odone, (nb - 1) & 1);
+    mbar_wait(bar_pempty((nb - 1) & 1), ((nb - 1) >> 1) & 1);  // PV_{nb-1} done
     tc_fence_after();
     const float inv = valid ? 1.f / l : 0.f;
     const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD;
@@ -503,6 +581,10 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   prm.n_ctx = (int)n_ctx;
   prm.n_qblocks = (int)((A + prm.QB - 1) / prm.QB);
   prm.scale_log2 = (float)(scale * 1.4426950408889634);
+  prm.lazy_thresh = LAZY_THRESH;
+  prm.poly_mask = POLY_MASK;
+  if (const char* e = getenv("CT_TC_LAZY")) prm.lazy_thresh = (float)atof(e);
+  if (const char* e = getenv("CT_TC_POLY")) prm.poly_mask = (uint32_t)strtoul(e, nullptr, 0);
   const size_t smem = Smem::TOTAL + 1024;
   CT_CUDA(cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));

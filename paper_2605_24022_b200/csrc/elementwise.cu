@@ -50,6 +50,84 @@ residual_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta, int
       x[row * cols + c] = from_f32<TX>(hr[c] * inv);
 }
 
+// Vectorised residual + RMSNorm: one CTA per row, the row held in registers
+// (float4 per thread-slot), so h and delta are read once and h, x written once.
+template <int VPT, typename TX>
+__global__ void __launch_bounds__(256)
+residual_rmsnorm_vec_kernel(float* __restrict__ h, const float* __restrict__ delta, int64_t cols,
+                            double eps, TX* __restrict__ x) {
+  const int64_t row = blockIdx.x;
+  float4* hr = reinterpret_cast<float4*>(h + row * cols);
+  const float4* dr = delta ? reinterpret_cast<const float4*>(delta + row * cols) : nullptr;
+  const int nv = (int)(cols / 4);
+  float4 v[VPT];
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < nv) {
+      float4 a = hr[c];
+      if (dr) {
+        const float4 d = __ldg(dr + c);
+        a.x += d.x; a.y += d.y; a.z += d.z; a.w += d.w;
+        hr[c] = a;
+      }
+      v[i] = a;
+      ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
+    }
+  }
+  __shared__ float red[8];
+  for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = (float)(1.0 / sqrt((double)tot / (double)cols + eps));
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const int c = threadIdx.x + i * 256;
+    if (c < nv) {
+      TX* xo = x + row * cols + 4 * (int64_t)c;
+      if constexpr (sizeof(TX) == 2) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v[i].x * inv, v[i].y * inv);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(v[i].z * inv, v[i].w * inv);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(xo) = u;
+      } else {
+        *reinterpret_cast<float4*>(xo) = make_float4(v[i].x * inv, v[i].y * inv, v[i].z * inv,
+                                                     v[i].w * inv);
+      }
+    }
+  }
+}
+
+// SwiGLU on 8-wide bf16 vectors: act = silu(gate) * up.
+__global__ void swiglu_vec_kernel(const uint4* __restrict__ gu, int64_t A, int64_t inter8,
+                                  uint4* __restrict__ act) {
+  const int64_t total = A * inter8;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = t / inter8, i = t % inter8;
+    const uint4 g = __ldg(gu + a * 2 * inter8 + i);
+    const uint4 u = __ldg(gu + a * 2 * inter8 + inter8 + i);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 gf = __bfloat1622float2(g2[k]);
+      const float2 uf = __bfloat1622float2(u2[k]);
+      o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
+                                    gf.y / (1.f + __expf(-gf.y)) * uf.y);
+    }
+    act[t] = o;
+  }
+}
+
 template <typename TI, typename TO>
 __global__ void mlp_act_kernel(const TI* __restrict__ gu, int64_t A, int64_t inter, int kind,
                                TO* __restrict__ act) {
@@ -113,6 +191,24 @@ extern "C" int ct_residual_rmsnorm(float* h, const void* delta, int delta_dtype,
   if (!valid_dtype(delta_dtype) || !valid_dtype(x_dtype)) return fail(CT_ERR_PARAM, "dtype");
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned g = (unsigned)A;
+  const bool aligned = ((uintptr_t)h % 16 == 0) && ((uintptr_t)delta % 16 == 0) &&
+                       ((uintptr_t)x_out % 16 == 0) && x_out != nullptr;
+  if (delta_dtype == CT_F32 && cols % 4 == 0 && cols <= 4 * 256 * 8 && aligned) {
+    const int vpt = (int)((cols / 4 + 255) / 256);
+#define CT_RMS(V)                                                                                  \
+  if (vpt <= V) {                                                                                  \
+    if (x_dtype == CT_BF16)                                                                        \
+      residual_rmsnorm_vec_kernel<V, __nv_bfloat16><<<g, 256, 0, st>>>(h, (const float*)delta,     \
+                                                                       cols, eps,                  \
+                                                                       (__nv_bfloat16*)x_out);     \
+    else                                                                                           \
+      residual_rmsnorm_vec_kernel<V, float><<<g, 256, 0, st>>>(h, (const float*)delta, cols, eps,  \
+                                                               (float*)x_out);                     \
+    return check_launch("residual_rmsnorm_vec_kernel");                                            \
+  }
+    CT_RMS(1) CT_RMS(2) CT_RMS(4) CT_RMS(8)
+#undef CT_RMS
+  }
   if (delta_dtype == CT_F32 && x_dtype == CT_F32)
     residual_rmsnorm_kernel<float, float><<<g, 256, 0, st>>>(h, (const float*)delta, cols, eps, (float*)x_out);
   else if (delta_dtype == CT_F32 && x_dtype == CT_BF16)
@@ -130,6 +226,12 @@ extern "C" int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype
   if (kind != 0 && kind != 1) return fail(CT_ERR_PARAM, "mlp kind %d", kind);
   cudaStream_t st = (cudaStream_t)stream;
   const unsigned g = grid_cap(A * inter);
+  if (kind == 0 && in_dtype == CT_BF16 && act_dtype == CT_BF16 && inter % 8 == 0 &&
+      ((uintptr_t)gu % 16 == 0) && ((uintptr_t)act % 16 == 0)) {
+    swiglu_vec_kernel<<<grid_cap(A * inter / 8), 256, 0, st>>>((const uint4*)gu, A, inter / 8,
+                                                                (uint4*)act);
+    return check_launch("swiglu_vec_kernel");
+  }
   if (in_dtype == CT_F32 && act_dtype == CT_F32)
     mlp_act_kernel<float, float><<<g, 256, 0, st>>>((const float*)gu, A, inter, kind, (float*)act);
   else if (in_dtype == CT_BF16 && act_dtype == CT_BF16)
