@@ -11,8 +11,9 @@
 //                  exp2, lazy max (rescale O only when the max grows > 2^8),
 //                  P (bf16) written swizzled to smem
 //   O += P V       tcgen05.mma  M128 N128 K16 x8, A=P smem, B=V smem (MN-major)
-// Warp roles: warps 0-3 softmax/epilogue (TMEM lanes 0-127), warp 4 TMA
-// producer, warp 5 MMA issuer (+TMEM alloc).  S is double buffered in TMEM,
+// Warp roles: warps 0-7 softmax/epilogue (two warps per TMEM lane quarter,
+// each owning half of the key columns), warp 8 TMA producer, warp 9 MMA
+// issuer (+TMEM alloc).  S is double buffered in TMEM,
 // P double buffered in smem, K/V flow through a 3-slot TMA ring.
 #include "common.cuh"
 
@@ -27,7 +28,10 @@ constexpr int TILE_M = 128;   // TMEM lanes / MMA M
 constexpr int BLK_N = 128;    // keys per block
 constexpr int HD = 128;       // head dim
 constexpr int KV_SLOTS = 3;
-constexpr int THREADS = 192;
+constexpr int SOFTMAX_WARPS = 8;
+constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
+constexpr int THREADS = 32 * (SOFTMAX_WARPS + 2);
+constexpr int HALF = BLK_N / 2;      // key columns per softmax thread
 constexpr int ATOM_BYTES = 128 * 64 * 2;      // [128 rows][64 bf16] swizzle-128B half tile
 constexpr int TILE_BYTES = 2 * ATOM_BYTES;    // 32 KiB: 128 rows x 128 bf16
 constexpr float LAZY_THRESH = 8.0f;           // log2 units
@@ -39,7 +43,8 @@ struct Smem {
   static constexpr int P = KV + KV_SLOTS * TILE_BYTES;
   static constexpr int BAR = P + 2 * TILE_BYTES;
   static constexpr int NBAR = 16;
-  static constexpr int TMEM_PTR = BAR + NBAR * 8;
+  static constexpr int XCH = BAR + NBAR * 8;          // [3][2][128] f32 max/sum exchange
+  static constexpr int TMEM_PTR = XCH + 3 * 2 * 128 * 4;
   static constexpr int TOTAL = TMEM_PTR + 16;
 };
 
@@ -201,8 +206,8 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, uint32_t& o0, uint32_t& 
   o0 = (uint32_t)pp + ((uint32_t)t << 23);
   o1 = (uint32_t)(pp >> 32) + ((uint32_t)(t >> 32) << 23);
 }
-// 16 chunks of 8 scores per block; these 6 use the polynomial (~37%).
-constexpr uint32_t POLY_MASK = (1u << 1) | (1u << 4) | (1u << 7) | (1u << 9) | (1u << 12) | (1u << 15);
+// Which of a thread's 8 chunks of 8 scores take the FMA-pipe polynomial
+// instead of MUFU.ex2 (template parameter; 0 = all MUFU).
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -218,9 +223,9 @@ struct Params {
   int n_qblocks;
   float scale_log2;
   float lazy_thresh;
-  uint32_t poly_mask;
 };
 
+template <uint32_t POLY_MASK>
 __global__ void __launch_bounds__(THREADS, 1)
 attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
@@ -266,14 +271,14 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(bar_sfull(b), 1);
-      mbar_init(bar_sempty(b), 128);
-      mbar_init(bar_pfull(b), 128);
+      mbar_init(bar_sempty(b), 32 * SOFTMAX_WARPS);
+      mbar_init(bar_pfull(b), 32 * SOFTMAX_WARPS);
       mbar_init(bar_pempty(b), 1);
     }
     mbar_init(bar_odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 5) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      su32(tmem_ptr)),
                  "r"(512)
@@ -287,7 +292,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
   const uint32_t tS[2] = {tbase + 0, tbase + 128};
   const uint32_t tO = tbase + 256;
 
-  if (warp == 4) {
+  if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       mbar_expect_tx(bar_q, TILE_BYTES);
@@ -310,7 +315,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         load(&map_v, j);
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       constexpr uint32_t IDESC_S = idesc_bf16(false);
@@ -358,93 +363,83 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax (rows)
-    const int m = threadIdx.x;  // TMEM lane / tile row
+    // ------------------------------------------------------------ softmax
+    // 8 warps: warp w owns TMEM lanes 32*(w%4).. (tile rows) and the column
+    // half hf = w/4 (keys 64*hf .. +63 of each block, O columns likewise), so
+    // every SMSP runs two softmax warps.  The two halves of a row agree on the
+    // running max through a double-buffered smem exchange + named barrier.
+    const int hf = warp >> 2;
+    const int m = (warp & 3) * 32 + lane;  // TMEM lane / tile row
     const int qi = m / p.G, hj = m % p.G;
     const int a = a0 + qi;
     const bool valid = a < p.A;
     const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
-    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    const uint32_t lane_off = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF);
+    float* xch = reinterpret_cast<float*>(gbase + Smem::XCH);  // [3][2][128]
     float m_used = -INFINITY, l = 0.f;
-    uint32_t r[BLK_N];
+    uint32_t r[HALF];
     for (int j = 0; j < nb; ++j) {
       const int b = j & 1;
       mbar_wait(bar_sfull(b), (j >> 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < BLK_N / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, r + c * 32);
+      for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, r + c * 32);
 #pragma unroll
-      for (int c = 0; c < BLK_N / 32; ++c) tmem_wait_ld32(r + c * 32);
+      for (int c = 0; c < HALF / 32; ++c) tmem_wait_ld32(r + c * 32);
       tc_fence_before();
       mbar_arrive(bar_sempty(b));
-      const int kbase = j * BLK_N;
-      const bool need_mask = kbase + BLK_N - 1 > pos;
+      const int kbase = j * BLK_N + hf * HALF;
+      const bool need_mask = kbase + HALF - 1 > pos;
       if (need_mask) {
 #pragma unroll
-        for (int c = 0; c < BLK_N; ++c)
+        for (int c = 0; c < HALF; ++c)
           if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
       }
-      // row max of the raw scores (scale > 0 commutes with max): 4 FMNMX3 chains
+      // row max of the raw scores (scale > 0 commutes with max)
       float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < BLK_N; c += 8) {
+      for (int c = 0; c < HALF; c += 8) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
       }
-      const float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
+      const float pm = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3]));
+      float* xb = xch + (j & 1) * 256;
+      xb[hf * 128 + m] = pm;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float mx = fmaxf(pm, xb[(hf ^ 1) * 128 + m]) * p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
       const bool grow = m_new > m_used + p.lazy_thresh;
-      // warp-uniform decision: tcgen05.ld/st are .sync.aligned
-      if (__any_sync(0xffffffffu, grow)) {
-        const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
-        if (j > 0) {
-          // rescale O in TMEM once PV_{j-1} has landed
-          // PV_{j-1} done.  Wait on its P-buffer barrier: this thread already
-          // waited that barrier's previous phase (PV_{j-3}), so the parity test
-          // cannot alias (a shared "O done" barrier could be 2 phases behind).
-          mbar_wait(bar_pempty((j - 1) & 1), ((j - 1) >> 1) & 1);
-          tc_fence_after();
-#pragma unroll 1
-          for (int c = 0; c < HD / 32; ++c) {
-            uint32_t o[32];
-            tmem_ld32(tO + lane_off + c * 32, o);
-            tmem_wait_ld32(o);
-#pragma unroll
-            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-            tmem_st32(tO + lane_off + c * 32, o);
-          }
-          tmem_wait_st();
-        }
-        l *= corr;
-        if (grow) m_used = m_new;
-      }
-      // P_j into smem buffer b (K-major SW128: row m, 16-B chunk c^(m&7)).
-      // x = s*scale - m (FFMA2); 2^x on MUFU for most chunks and on the FMA
-      // pipe (degree-3 polynomial) for POLY_MASK chunks to balance the pipes.
+      // warp-uniform decision (tcgen05.ld/st are .sync.aligned).  P_j is built
+      // with the new max first; the O rescale (which must wait for PV_{j-1})
+      // runs after P_j is in smem so it overlaps PV_{j-1} instead of stalling.
+      const bool any_grow = __any_sync(0xffffffffu, grow);
+      const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
+      if (grow) m_used = m_new;
+      // P_j half-row into smem buffer b: atom hf (K-major SW128, chunk c^(m&7))
       if (j >= 2) mbar_wait(bar_pempty(b), ((j >> 1) - 1) & 1);
-      uint8_t* prow = gP + b * TILE_BYTES + m * 128;
+      uint8_t* prow = gP + b * TILE_BYTES + hf * ATOM_BYTES + m * 128;
       const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
       const uint64_t nm2 = pk2(-m_used, -m_used);
       uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
 #pragma unroll
-      for (int ch = 0; ch < BLK_N / 8; ++ch) {
+      for (int ch = 0; ch < HALF / 8; ++ch) {
         uint64_t x2[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           x2[t] = ffma2(pk2(__uint_as_float(r[ch * 8 + 2 * t]), __uint_as_float(r[ch * 8 + 2 * t + 1])),
                         sc2, nm2);
         uint32_t e[8];
-        if (((p.poly_mask >> ch) & 1) && !need_mask) {
+        if (((POLY_MASK >> ch) & 1) && !need_mask) {
 #pragma unroll
           for (int t = 0; t < 4; ++t) exp2_poly2(x2[t], e[2 * t], e[2 * t + 1]);
         } else {
 #pragma unroll
           for (int t = 0; t < 4; ++t) {
-            float a, bb;
-            upk2(x2[t], a, bb);
-            e[2 * t] = __float_as_uint(ex2(a));
-            e[2 * t + 1] = __float_as_uint(ex2(bb));
+            float x0, x1;
+            upk2(x2[t], x0, x1);
+            e[2 * t] = __float_as_uint(ex2(x0));
+            e[2 * t + 1] = __float_as_uint(ex2(x1));
           }
         }
 #pragma unroll
@@ -455,26 +450,45 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         v.y = pack_bf16(__uint_as_float(e[2]), __uint_as_float(e[3]));
         v.z = pack_bf16(__uint_as_float(e[4]), __uint_as_float(e[5]));
         v.w = pack_bf16(__uint_as_float(e[6]), __uint_as_float(e[7]));
-        const int atom = ch >> 3, c8 = ch & 7;
-        *reinterpret_cast<uint4*>(prow + atom * ATOM_BYTES + ((c8 ^ (m & 7)) << 4)) = v;
+        *reinterpret_cast<uint4*>(prow + ((ch ^ (m & 7)) << 4)) = v;
       }
       {
         float s0, s1, s2, s3;
         upk2(acc2[0], s0, s1);
         upk2(acc2[1], s2, s3);
-        l += (s0 + s1) + (s2 + s3);
+        l = l * corr + ((s0 + s1) + (s2 + s3));  // partial row sum over this half
       }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      if (any_grow && j > 0) {
+        // O[:, half] *= corr once PV_{j-1} has landed.  Wait on PV_{j-1}'s
+        // P-buffer barrier: this thread already waited that barrier's previous
+        // phase (PV_{j-3}), so the parity test cannot alias.
+        mbar_wait(bar_pempty((j - 1) & 1), ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < HALF / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO + lane_off + c * 32, o);
+          tmem_wait_ld32(o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+          tmem_st32(tO + lane_off + c * 32, o);
+        }
+        tmem_wait_st();
+      }
       tc_fence_before();
       mbar_arrive(bar_pfull(b));
     }
-    // epilogue: O / l -> global
+    // epilogue: combine the two partial row sums, O[:, half] / l -> global
+    xch[512 + hf * 128 + m] = l;
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    l += xch[512 + (hf ^ 1) * 128 + m];
     mbar_wait(bar_pempty((nb - 1) & 1), ((nb - 1) >> 1) & 1);  // PV_{nb-1} done
     tc_fence_after();
     const float inv = valid ? 1.f / l : 0.f;
-    const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD;
+    const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD + hf * HALF;
 #pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int c = 0; c < HALF / 32; ++c) {
       uint32_t o[32];
       tmem_ld32(tO + lane_off + c * 32, o);
       tmem_wait_ld32(o);
@@ -502,7 +516,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) {
+  if (warp == MMA_WARP) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
                  : "memory");
@@ -582,14 +596,15 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   prm.n_qblocks = (int)((A + prm.QB - 1) / prm.QB);
   prm.scale_log2 = (float)(scale * 1.4426950408889634);
   prm.lazy_thresh = LAZY_THRESH;
-  prm.poly_mask = POLY_MASK;
   if (const char* e = getenv("CT_TC_LAZY")) prm.lazy_thresh = (float)atof(e);
-  if (const char* e = getenv("CT_TC_POLY")) prm.poly_mask = (uint32_t)strtoul(e, nullptr, 0);
   const size_t smem = Smem::TOTAL + 1024;
-  CT_CUDA(cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)smem));
+  uint32_t poly = 0;
+  if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
+  auto kern = poly == 0x22 ? attention_tc_kernel<0x22> : poly == 0x92 ? attention_tc_kernel<0x92>
+                                                                      : attention_tc_kernel<0>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)(prm.n_qblocks * Hkv);
-  attention_tc_kernel<<<grid, THREADS, smem, st>>>(mq, mk, mv, prm);
+  kern<<<grid, THREADS, smem, st>>>(mq, mk, mv, prm);
   return check_launch("attention_tc_kernel");
 }
 
