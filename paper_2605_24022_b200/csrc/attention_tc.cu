@@ -27,11 +27,9 @@ namespace tc {
 constexpr int TILE_M = 128;   // TMEM lanes / MMA M
 constexpr int BLK_N = 128;    // keys per block
 constexpr int HD = 128;       // head dim
-constexpr int KV_SLOTS = 3;
-constexpr int SOFTMAX_WARPS = 8;
-constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
-constexpr int THREADS = 32 * (SOFTMAX_WARPS + 2);
-constexpr int HALF = BLK_N / 2;      // key columns per softmax thread
+constexpr int KV_SLOTS = 5;
+constexpr int MAX_SPLIT = 4;
+constexpr int NSB = 3;               // S/P TMEM buffers        // softmax threads per tile row (key-column split)
 constexpr int ATOM_BYTES = 128 * 64 * 2;      // [128 rows][64 bf16] swizzle-128B half tile
 constexpr int TILE_BYTES = 2 * ATOM_BYTES;    // 32 KiB: 128 rows x 128 bf16
 constexpr float LAZY_THRESH = 8.0f;           // log2 units
@@ -40,11 +38,10 @@ struct Smem {
   // offsets from the 1024-aligned base
   static constexpr int Q = 0;
   static constexpr int KV = Q + TILE_BYTES;
-  static constexpr int P = KV + KV_SLOTS * TILE_BYTES;
-  static constexpr int BAR = P + 2 * TILE_BYTES;
-  static constexpr int NBAR = 16;
-  static constexpr int XCH = BAR + NBAR * 8;          // [3][2][128] f32 max/sum exchange
-  static constexpr int TMEM_PTR = XCH + 3 * 2 * 128 * 4;
+  static constexpr int BAR = KV + KV_SLOTS * TILE_BYTES;
+  static constexpr int NBAR = 1 + 2 * KV_SLOTS + 8;
+  static constexpr int XCH = BAR + NBAR * 8;  // [3][MAX_SPLIT][128] f32 max/sum exchange
+  static constexpr int TMEM_PTR = XCH + 3 * MAX_SPLIT * 128 * 4;
   static constexpr int TOTAL = TMEM_PTR + 16;
 };
 
@@ -98,6 +95,26 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t adesc, uint64_t
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+
+// A operand from TMEM (.kind::f16, A K-major packed bf16x2 along columns).
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t* r) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+      "r"(r[15])
       : "memory");
 }
 
@@ -225,27 +242,30 @@ struct Params {
   float lazy_thresh;
 };
 
-template <uint32_t POLY_MASK>
-__global__ void __launch_bounds__(THREADS, 1)
+template <int NSPLIT, uint32_t POLY_MASK>
+__global__ void __launch_bounds__(32 * (4 * NSPLIT + 2), 1)
 attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const Params p) {
+  constexpr int SOFTMAX_WARPS = 4 * NSPLIT;
+  constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
+  constexpr int HALF = BLK_N / NSPLIT;  // key columns per softmax thread
+  constexpr int NSM = 32 * SOFTMAX_WARPS;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sQ = base + Smem::Q, sKV = base + Smem::KV, sP = base + Smem::P;
-  uint8_t* gP = gbase + Smem::P;
+  const uint32_t sQ = base + Smem::Q, sKV = base + Smem::KV;
   const uint32_t bar0 = base + Smem::BAR;
   // barriers
   const uint32_t bar_q = bar0 + 0 * 8;
-  auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };            // 3
-  auto bar_empty = [&](int s) { return bar0 + (4 + s) * 8; };           // 3
-  auto bar_sfull = [&](int b) { return bar0 + (7 + b) * 8; };           // 2
-  auto bar_sempty = [&](int b) { return bar0 + (9 + b) * 8; };          // 2
-  auto bar_pfull = [&](int b) { return bar0 + (11 + b) * 8; };          // 2
-  auto bar_pempty = [&](int b) { return bar0 + (13 + b) * 8; };         // 2
-  const uint32_t bar_odone = bar0 + 15 * 8;
+  auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };
+  auto bar_empty = [&](int s) { return bar0 + (1 + KV_SLOTS + s) * 8; };
+  constexpr int B2 = 1 + 2 * KV_SLOTS;
+  // per S/P TMEM buffer (3): S landed, P written, PV (the reader of P) done
+  auto bar_sfull = [&](int b) { return bar0 + (B2 + b) * 8; };
+  auto bar_pfull = [&](int b) { return bar0 + (B2 + 3 + b) * 8; };
+  auto bar_pvdone = [&](int b) { return bar0 + (B2 + 6 + b) * 8; };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + Smem::TMEM_PTR);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -269,13 +289,11 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       mbar_init(bar_full(s), 1);
       mbar_init(bar_empty(s), 1);
     }
-    for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < NSB; ++b) {
       mbar_init(bar_sfull(b), 1);
-      mbar_init(bar_sempty(b), 32 * SOFTMAX_WARPS);
-      mbar_init(bar_pfull(b), 32 * SOFTMAX_WARPS);
-      mbar_init(bar_pempty(b), 1);
+      mbar_init(bar_pfull(b), NSM);
+      mbar_init(bar_pvdone(b), 1);
     }
-    mbar_init(bar_odone, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -289,8 +307,12 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
   __syncthreads();
   tc_fence_after();
   const uint32_t tbase = *tmem_ptr;
-  const uint32_t tS[2] = {tbase + 0, tbase + 128};
-  const uint32_t tO = tbase + 256;
+  // TMEM: three S buffers (128 fp32 columns each) + O (128).  P_j (bf16x2,
+  // 64 columns) overwrites the first half of S_j's buffer once the softmax
+  // has read S_j; the PV MMA reads it as its TMEM A operand, so P never
+  // touches shared memory.  Three buffers let S run two blocks ahead.
+  auto tS = [&](int b) { return tbase + (uint32_t)(b * 128); };
+  const uint32_t tO = tbase + 384;
 
   if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA producer
@@ -325,15 +347,16 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       int slot = 0;
       uint32_t phase = 0;
       auto issue_s = [&](int j) {
-        const int b = j & 1;
-        if (j >= 2) mbar_wait(bar_sempty(b), ((j >> 1) - 1) & 1);
+        const int b = j % NSB;
+        // buffer b last held P_{j-3}: wait for its reader PV_{j-3}
+        if (j >= NSB) mbar_wait(bar_pvdone(b), ((j / NSB) - 1) & 1);
         mbar_wait(bar_full(slot), phase);
         tc_fence_after();
         const uint32_t k_tile = sKV + slot * TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
-          tc_mma(tS[b], sdesc(sQ + off, 16, 1024), sdesc(k_tile + off, 16, 1024), IDESC_S,
+          tc_mma(tS(b), sdesc(sQ + off, 16, 1024), sdesc(k_tile + off, 16, 1024), IDESC_S,
                  kk > 0);
         }
         tc_commit(bar_empty(slot));
@@ -341,25 +364,25 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
       };
       issue_s(0);
+      if (nb > 1) issue_s(1);
       for (int j = 0; j < nb; ++j) {
-        if (j + 1 < nb) issue_s(j + 1);
         // O += P_j V_j
-        const int b = j & 1;
-        mbar_wait(bar_pfull(b), (j >> 1) & 1);
+        const int b = j % NSB;
+        mbar_wait(bar_pfull(b), (j / NSB) & 1);
         mbar_wait(bar_full(slot), phase);
         tc_fence_after();
         const uint32_t v_tile = sKV + slot * TILE_BYTES;
-        const uint32_t p_tile = sP + b * TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < BLK_N / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
-          // V: MN-major, K-step of 16 keys = 2 x 1024 B core-matrix groups
-          tc_mma(tO, sdesc(p_tile + aoff, 16, 1024), sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024),
-                 IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
+          // A = P from TMEM (16 keys = 8 packed columns); B = V, MN-major,
+          // K-step of 16 keys = 2 x 1024 B core-matrix groups
+          tc_mma_ts(tO, tS(b) + kk * 8, sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024), IDESC_O,
+                    (j > 0 || kk > 0) ? 1u : 0u);
         }
         tc_commit(bar_empty(slot));
-        tc_commit(bar_pempty(b));
+        tc_commit(bar_pvdone(b));
         if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
+        if (j + 2 < nb) issue_s(j + 2);
       }
     }
   } else {
@@ -375,19 +398,18 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
     const bool valid = a < p.A;
     const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
     const uint32_t lane_off = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF);
+    const uint32_t lane_off_p = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF / 2);
     float* xch = reinterpret_cast<float*>(gbase + Smem::XCH);  // [3][2][128]
     float m_used = -INFINITY, l = 0.f;
     uint32_t r[HALF];
     for (int j = 0; j < nb; ++j) {
-      const int b = j & 1;
-      mbar_wait(bar_sfull(b), (j >> 1) & 1);
+      const int b = j % NSB;
+      mbar_wait(bar_sfull(b), (j / NSB) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, r + c * 32);
+      for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS(b) + lane_off + c * 32, r + c * 32);
 #pragma unroll
       for (int c = 0; c < HALF / 32; ++c) tmem_wait_ld32(r + c * 32);
-      tc_fence_before();
-      mbar_arrive(bar_sempty(b));
       const int kbase = j * BLK_N + hf * HALF;
       const bool need_mask = kbase + HALF - 1 > pos;
       if (need_mask) {
@@ -404,10 +426,19 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
           mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
       }
       const float pm = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3]));
-      float* xb = xch + (j & 1) * 256;
-      xb[hf * 128 + m] = pm;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      const float mx = fmaxf(pm, xb[(hf ^ 1) * 128 + m]) * p.scale_log2;
+      float* xb = xch + (j & 1) * (NSPLIT * 128);
+      float mrow = pm;
+      if constexpr (NSPLIT > 1) {
+        xb[hf * 128 + m] = pm;
+        // also orders every half's S_j reads before any half's P_j writes
+        // (P_j aliases the first half of S_j's TMEM columns)
+        tc_fence_before();
+        asm volatile("bar.sync 1, %0;" ::"n"(NSM) : "memory");
+        tc_fence_after();
+#pragma unroll
+        for (int o = 1; o < NSPLIT; ++o) mrow = fmaxf(mrow, xb[((hf + o) % NSPLIT) * 128 + m]);
+      }
+      const float mx = mrow * p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
       const bool grow = m_new > m_used + p.lazy_thresh;
       // warp-uniform decision (tcgen05.ld/st are .sync.aligned).  P_j is built
@@ -417,8 +448,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
       if (grow) m_used = m_new;
       // P_j half-row into smem buffer b: atom hf (K-major SW128, chunk c^(m&7))
-      if (j >= 2) mbar_wait(bar_pempty(b), ((j >> 1) - 1) & 1);
-      uint8_t* prow = gP + b * TILE_BYTES + hf * ATOM_BYTES + m * 128;
+      uint32_t pk[HALF / 2];  // packed bf16x2 P for this thread's key columns
       const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
       const uint64_t nm2 = pk2(-m_used, -m_used);
       uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
@@ -445,12 +475,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e[2 * t] | ((uint64_t)e[2 * t + 1] << 32));
-        uint4 v;
-        v.x = pack_bf16(__uint_as_float(e[0]), __uint_as_float(e[1]));
-        v.y = pack_bf16(__uint_as_float(e[2]), __uint_as_float(e[3]));
-        v.z = pack_bf16(__uint_as_float(e[4]), __uint_as_float(e[5]));
-        v.w = pack_bf16(__uint_as_float(e[6]), __uint_as_float(e[7]));
-        *reinterpret_cast<uint4*>(prow + ((ch ^ (m & 7)) << 4)) = v;
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          pk[ch * 4 + t] = pack_bf16(__uint_as_float(e[2 * t]), __uint_as_float(e[2 * t + 1]));
       }
       {
         float s0, s1, s2, s3;
@@ -458,12 +485,16 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         upk2(acc2[1], s2, s3);
         l = l * corr + ((s0 + s1) + (s2 + s3));  // partial row sum over this half
       }
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      // P_j -> TMEM columns [hf*HALF/2, +HALF/2) of P buffer b (lane m)
+#pragma unroll
+      for (int c = 0; c < HALF / 64; ++c) tmem_st32(tS(b) + lane_off_p + c * 32, pk + c * 32);
+      if constexpr (HALF / 2 < 32) tmem_st16(tS(b) + lane_off_p, pk);
+      tmem_wait_st();
       if (any_grow && j > 0) {
-        // O[:, half] *= corr once PV_{j-1} has landed.  Wait on PV_{j-1}'s
-        // P-buffer barrier: this thread already waited that barrier's previous
-        // phase (PV_{j-3}), so the parity test cannot alias.
-        mbar_wait(bar_pempty((j - 1) & 1), ((j - 1) >> 1) & 1);
+        // O[:, half] *= corr once PV_{j-1} has landed.  The parity test on
+        // buffer (j-1)%3's barrier cannot alias: its previous phase (PV_{j-4})
+        // completed before S_j was issued into buffer j%3 (in-order pipe).
+        mbar_wait(bar_pvdone((j - 1) % NSB), ((j - 1) / NSB) & 1);
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < HALF / 32; ++c) {
@@ -480,10 +511,16 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       mbar_arrive(bar_pfull(b));
     }
     // epilogue: combine the two partial row sums, O[:, half] / l -> global
-    xch[512 + hf * 128 + m] = l;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    l += xch[512 + (hf ^ 1) * 128 + m];
-    mbar_wait(bar_pempty((nb - 1) & 1), ((nb - 1) >> 1) & 1);  // PV_{nb-1} done
+    if constexpr (NSPLIT > 1) {
+      float* xl = xch + 2 * NSPLIT * 128;
+      xl[hf * 128 + m] = l;
+      asm volatile("bar.sync 1, %0;" ::"n"(NSM) : "memory");
+      float lt = 0.f;
+#pragma unroll
+      for (int o = 0; o < NSPLIT; ++o) lt += xl[o * 128 + m];
+      l = lt;
+    }
+    mbar_wait(bar_pvdone((nb - 1) % NSB), ((nb - 1) / NSB) & 1);  // PV_{nb-1} done
     tc_fence_after();
     const float inv = valid ? 1.f / l : 0.f;
     const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD + hf * HALF;
@@ -598,13 +635,16 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   prm.lazy_thresh = LAZY_THRESH;
   if (const char* e = getenv("CT_TC_LAZY")) prm.lazy_thresh = (float)atof(e);
   const size_t smem = Smem::TOTAL + 1024;
+  int split = 2;
+  if (const char* e = getenv("CT_TC_SPLIT")) split = atoi(e);
   uint32_t poly = 0;
   if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
-  auto kern = poly == 0x22 ? attention_tc_kernel<0x22> : poly == 0x92 ? attention_tc_kernel<0x92>
-                                                                      : attention_tc_kernel<0>;
+  auto kern = split == 4 ? attention_tc_kernel<4, 0> : split == 1 ? attention_tc_kernel<1, 0>
+            : poly == 0x22 ? attention_tc_kernel<2, 0x22> : attention_tc_kernel<2, 0>;
+  const int threads = 32 * (4 * (split == 4 ? 4 : split == 1 ? 1 : 2) + 2);
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)(prm.n_qblocks * Hkv);
-  kern<<<grid, THREADS, smem, st>>>(mq, mk, mv, prm);
+  kern<<<grid, threads, smem, st>>>(mq, mk, mv, prm);
   return check_launch("attention_tc_kernel");
 }
 
