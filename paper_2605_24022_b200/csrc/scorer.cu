@@ -78,7 +78,7 @@ template <typename T> struct ScoreCfg;
 template <> struct ScoreCfg<double> { static constexpr int POINTS = 8192; };
 template <> struct ScoreCfg<float> { static constexpr int POINTS = 16384; };
 
-constexpr int SCORE_THREADS = 512;
+constexpr int SCORE_THREADS = 1024;
 constexpr int LANE_BLOCK = 128;
 
 __host__ __device__ constexpr int pass_radix(int logn, int p) {
@@ -87,13 +87,19 @@ __host__ __device__ constexpr int pass_radix(int logn, int p) {
 }
 __host__ __device__ constexpr int num_passes(int logn) { return logn / 3 + (logn % 3 ? 1 : 0); }
 
+// Shared-memory signal index with one pad element per 8: keeps the stride-R
+// stores of the first Stockham pass off a single bank.
+__device__ __forceinline__ int spad(int i) { return i + (i >> 3); }
+
 template <typename IN>
 __device__ __forceinline__ double load_as_double(const IN* p) { return (double)to_f32(*p); }
 __device__ __forceinline__ double load_as_double(const float* p) { return (double)*p; }
 
 // One Stockham pass over all S signals in shared memory (in place: every
-// thread loads all its butterflies, barrier, then stores).
-template <typename T, int LOGN, int R, bool INV, bool MASK>
+// thread loads all its butterflies, barrier, then stores).  MASK applies the
+// low-pass on the loaded (natural-order) bins; ENERGY stores |z|^2 into .x
+// instead of z (the last inverse pass feeds the per-token accumulation).
+template <typename T, int LOGN, int R, bool INV, bool MASK, bool ENERGY>
 __device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
                                               const cpx<T>* __restrict__ tw,
                                               int cutoff) {
@@ -103,17 +109,17 @@ __device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
   constexpr int BPT = (PTS / R + SCORE_THREADS - 1) / SCORE_THREADS;
   cpx<T> v[BPT][R];
   const int total = S * NB;
+  const int step = N / (Ns * R);
 #pragma unroll
   for (int k = 0; k < BPT; ++k) {
     const int b = threadIdx.x + k * SCORE_THREADS;
     if (b < total) {
-      const int s = b / NB, j = b % NB;
+      const int sg = b / NB, j = b % NB;
       const int jm = j % Ns;
-      const int step = N / (Ns * R);
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int idx = j + r * NB;
-        cpx<T> val = sig[s * N + idx];
+        cpx<T> val = sig[spad(sg * N + idx)];
         if (MASK) {
           const int kk = idx < N - idx ? idx : N - idx;
           if (kk >= cutoff) val = {(T)0, (T)0};
@@ -133,23 +139,18 @@ __device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
   for (int k = 0; k < BPT; ++k) {
     const int b = threadIdx.x + k * SCORE_THREADS;
     if (b < total) {
-      const int s = b / NB, j = b % NB;
+      const int sg = b / NB, j = b % NB;
       const int idxD = (j / Ns) * Ns * R + (j % Ns);
 #pragma unroll
-      for (int r = 0; r < R; ++r) sig[s * N + idxD + r * Ns] = v[k][r];
+      for (int r = 0; r < R; ++r) {
+        if (ENERGY)
+          sig[spad(sg * N + idxD + r * Ns)].x = v[k][r].x * v[k][r].x + v[k][r].y * v[k][r].y;
+        else
+          sig[spad(sg * N + idxD + r * Ns)] = v[k][r];
+      }
     }
   }
   __syncthreads();
-}
-
-template <typename T, int LOGN, int P, bool INV, bool MASK_FIRST>
-__device__ __forceinline__ void run_passes(cpx<T>* sig, int S, int Ns,
-                                           const cpx<T>* tw, int cutoff) {
-  if constexpr (P < num_passes(LOGN) - (INV ? 1 : 0)) {
-    constexpr int R = pass_radix(LOGN, P);
-    stockham_pass<T, LOGN, R, INV, MASK_FIRST && P == 0>(sig, S, Ns, tw, cutoff);
-    run_passes<T, LOGN, P + 1, INV, MASK_FIRST>(sig, S, Ns * R, tw, cutoff);
-  }
 }
 
 template <int LOGN, int P>
@@ -158,7 +159,20 @@ __host__ __device__ constexpr int ns_before() {
   else return ns_before<LOGN, P - 1>() * pass_radix(LOGN, P - 1);
 }
 
-// grid: x = lane block, y = tensor (0 K, 1 V), z = c*L + l
+template <typename T, int LOGN, int P, bool INV>
+__device__ __forceinline__ void run_passes(cpx<T>* sig, int S, const cpx<T>* tw, int cutoff) {
+  if constexpr (P < num_passes(LOGN)) {
+    constexpr int R = pass_radix(LOGN, P);
+    constexpr bool LAST = P == num_passes(LOGN) - 1;
+    stockham_pass<T, LOGN, R, INV, INV && P == 0, INV && LAST>(sig, S, ns_before<LOGN, P>(), tw,
+                                                               cutoff);
+    run_passes<T, LOGN, P + 1, INV>(sig, S, tw, cutoff);
+  }
+}
+
+// grid: x = lane block, y = tensor (0 K, 1 V), z = c*L + l.  Per lane group
+// (2S lanes): load -> forward FFT -> masked inverse FFT -> |recon|^2 in place
+// -> per-token sums over the S signals in fixed order into registers.
 template <typename T, typename IN, int LOGN>
 __global__ void __launch_bounds__(SCORE_THREADS, 1)
 fft_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
@@ -168,11 +182,7 @@ fft_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
   constexpr int N = 1 << LOGN;
   constexpr int PTS = ScoreCfg<T>::POINTS;
   constexpr int S = PTS / N < 1 ? 1 : (PTS / N > 64 ? 64 : PTS / N);
-  constexpr int NP = num_passes(LOGN);
-  constexpr int RL = pass_radix(LOGN, NP - 1);  // last pass radix
-  constexpr int NBL = N / RL;
-  constexpr int NSL = N / RL;                   // Ns of the last pass
-  constexpr int BPTL = (S * NBL + SCORE_THREADS - 1) / SCORE_THREADS;
+  constexpr int TPT = (N + SCORE_THREADS - 1) / SCORE_THREADS;  // tokens per thread
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cpx<T>* sig = reinterpret_cast<cpx<T>*>(smem_raw);
 
@@ -182,78 +192,73 @@ fft_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
   const int lane0 = lb * LANE_BLOCK;
   const int lane_end = min(lanes, lane0 + LANE_BLOCK);
 
-  double acc[BPTL][RL];
+  double acc[TPT];
 #pragma unroll
-  for (int k = 0; k < BPTL; ++k)
-#pragma unroll
-    for (int r = 0; r < RL; ++r) acc[k][r] = 0.0;
+  for (int i = 0; i < TPT; ++i) acc[i] = 0.0;
 
   for (int g0 = lane0; g0 < lane_end; g0 += 2 * S) {
-    // load 2S lanes of every token; consecutive threads walk lanes then tokens
-    for (int q = threadIdx.x; q < S * N; q += SCORE_THREADS) {
-      const int s = q % S, n = q / S;
-      const int la = g0 + 2 * s, lbn = la + 1;
+    // load 2S lanes of every token: one thread per (token, 8-lane slice) with
+    // a 16-B (bf16) / 2x16-B (f32) vector load when the slice is in range;
+    // smem writes are then contiguous per signal (conflict-free).
+    constexpr int SL = 4;  // signals per slice (8 lanes)
+    const bool vec_ok = ((ld_token * (int64_t)sizeof(IN)) % 16 == 0) &&
+                        (((uintptr_t)base) % 16 == 0) && (g0 % 8 == 0);
+    for (int q = threadIdx.x; q < (S / SL > 0 ? S / SL : 1) * N; q += SCORE_THREADS) {
+      const int n = q % N, sl = q / N;
       const IN* row = base + (int64_t)n * ld_token;
-      T re = la < lane_end ? (T)load_as_double(row + la) : (T)0;
-      T im = lbn < lane_end ? (T)load_as_double(row + lbn) : (T)0;
-      sig[s * N + n] = {re, im};
-    }
-    __syncthreads();
-    run_passes<T, LOGN, 0, false, false>(sig, S, 1, tw, cutoff);
-    run_passes<T, LOGN, 0, true, true>(sig, S, 1, tw, cutoff);
-    // last inverse pass: outputs go straight into per-token energy registers
-    {
-      constexpr int Ns = ns_before<LOGN, NP - 1>();
-      static_assert(Ns == NSL, "last pass span");
+      const int lbase = g0 + 8 * sl;
+      if (S >= SL && vec_ok && lbase + 8 <= lane_end) {
+        float f[8];
+        if constexpr (sizeof(IN) == 2) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(row + lbase));
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
 #pragma unroll
-      for (int k = 0; k < BPTL; ++k) {
-        const int b = threadIdx.x + k * SCORE_THREADS;
-        if (b < S * NBL) {
-          const int s = b / NBL, j = b % NBL;
-          cpx<T> v[RL];
-#pragma unroll
-          for (int r = 0; r < RL; ++r) {
-            const int idx = j + r * NBL;
-            cpx<T> val = sig[s * N + idx];
-            if (NP == 1) {  // single pass: it is also the masked first pass
-              const int kk = idx < N - idx ? idx : N - idx;
-              if (kk >= cutoff) val = {(T)0, (T)0};
-            }
-            if (r > 0 && j > 0) {
-              cpx<T> w = tw[j * r * (N / (Ns * RL))];
-              w.y = -w.y;
-              val = cmul(val, w);
-            }
-            v[r] = val;
+          for (int t = 0; t < 4; ++t) {
+            const float2 ff = __bfloat1622float2(h2[t]);
+            f[2 * t] = ff.x;
+            f[2 * t + 1] = ff.y;
           }
-          dft_small<RL, true>(v);
+        } else {
+          const float4 a = __ldg(reinterpret_cast<const float4*>(row + lbase));
+          const float4 b = __ldg(reinterpret_cast<const float4*>(row + lbase) + 1);
+          f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+          f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+        }
 #pragma unroll
-          for (int r = 0; r < RL; ++r)
-            acc[k][r] += (double)v[r].x * (double)v[r].x + (double)v[r].y * (double)v[r].y;
+        for (int t = 0; t < SL; ++t)
+          sig[spad((sl * SL + t) * N + n)] = {(T)f[2 * t], (T)f[2 * t + 1]};
+      } else {
+        const int smax = S >= SL ? SL : S;
+        for (int t = 0; t < smax; ++t) {
+          const int la = lbase + 2 * t, lbn = la + 1;
+          T re = la < lane_end ? (T)load_as_double(row + la) : (T)0;
+          T im = lbn < lane_end ? (T)load_as_double(row + lbn) : (T)0;
+          sig[spad((sl * SL + t) * N + n)] = {re, im};
         }
       }
     }
     __syncthreads();
-  }
-  // combine signal slots in fixed order: E[s][token] then sum over s
-  double* E = reinterpret_cast<double*>(smem_raw);
+    run_passes<T, LOGN, 0, false>(sig, S, tw, cutoff);
+    run_passes<T, LOGN, 0, true>(sig, S, tw, cutoff);
+    // energies now in sig[s][n].x: fixed-order sum over the group's signals
 #pragma unroll
-  for (int k = 0; k < BPTL; ++k) {
-    const int b = threadIdx.x + k * SCORE_THREADS;
-    if (b < S * NBL) {
-      const int s = b / NBL, j = b % NBL;
-#pragma unroll
-      for (int r = 0; r < RL; ++r) E[s * N + j + r * NBL] = acc[k][r];
+    for (int i = 0; i < TPT; ++i) {
+      const int n = threadIdx.x + i * SCORE_THREADS;
+      if (n < N) {
+        double e = 0.0;
+        for (int sg = 0; sg < S; ++sg) e += (double)sig[spad(sg * N + n)].x;
+        acc[i] += e;
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
   const double inv_n2 = 1.0 / ((double)N * (double)N);
   const int nlb = gridDim.x;
   double* out = partial + ((((int64_t)blockIdx.z * 2 + tensor) * nlb) + lb) * N;
-  for (int n = threadIdx.x; n < N; n += SCORE_THREADS) {
-    double e = 0.0;
-    for (int s = 0; s < S; ++s) e += E[s * N + n];
-    out[n] = e * inv_n2;
+#pragma unroll
+  for (int i = 0; i < TPT; ++i) {
+    const int n = threadIdx.x + i * SCORE_THREADS;
+    if (n < N) out[n] = acc[i] * inv_n2;
   }
 }
 
@@ -473,8 +478,7 @@ static int launch_fft_t(const void* k, const void* v, int L, int C, int lanes, i
   constexpr int N = 1 << LOGN;
   constexpr int PTS = ScoreCfg<T>::POINTS;
   constexpr int S = PTS / N < 1 ? 1 : (PTS / N > 64 ? 64 : PTS / N);
-  size_t smem = (size_t)S * N * sizeof(cpx<T>);
-  if (smem < (size_t)S * N * sizeof(double)) smem = (size_t)S * N * sizeof(double);
+  const size_t smem = (size_t)(S * N + S * N / 8 + 8) * sizeof(cpx<T>);  // padded (spad)
   auto kern = fft_energy_kernel<T, IN, LOGN>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const int nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
