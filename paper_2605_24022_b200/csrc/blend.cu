@@ -166,6 +166,128 @@ struct SegArray {
   ct_segment s[CT_MAX_SEGMENTS];
 };
 
+// Rotate the 4 adjacent pairs packed in a 16-B bf16 chunk with (cos, sin)[4].
+__device__ __forceinline__ uint4 rot8_bf16(uint4 u, const float4 c01, const float4 c23) {
+  __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+  const float cs[8] = {c01.x, c01.y, c01.z, c01.w, c23.x, c23.y, c23.z, c23.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const float2 f = __bfloat1622float2(h2[i]);
+    const float c = cs[2 * i], s = cs[2 * i + 1];
+    h2[i] = __floats2bfloat162_rn(f.x * c - f.y * s, f.x * s + f.y * c);
+  }
+  return u;
+}
+
+// Hot-path blend for bf16 caches with adjacent pairing: one 16-B chunk (8
+// elements = 4 rotation pairs of one head) per unit, UNR units per thread with
+// every load issued before any math so ~UNR x 64 B are in flight per thread.
+template <int UNR>
+__global__ void __launch_bounds__(256)
+blend_bf16_kernel(SegArray segs, int64_t src_row_stride, int upr, int cph,
+                  const float4* __restrict__ table, int half, __nv_bfloat16* __restrict__ kc,
+                  __nv_bfloat16* __restrict__ vc, int64_t cache_row_stride) {
+  const ct_segment sg = segs.s[blockIdx.y];
+  const int64_t total = sg.rows * upr;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(sg.k);
+  const __nv_bfloat16* vs = reinterpret_cast<const __nv_bfloat16*>(sg.v);
+  for (int64_t u0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u0 < total;
+       u0 += nthr * UNR) {
+    uint4 kr[UNR], vr[UNR];
+    float4 c0[UNR], c1[UNR];
+    int64_t dst[UNR];
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const int64_t u = u0 + k * nthr;
+      dst[k] = -1;
+      if (u < total) {
+        const int64_t row = u / upr;
+        const int w = (int)(u - row * upr);
+        const int32_t tk = __ldg(sg.tok + row);
+        const int64_t pos = sg.pos0 + tk;
+        const int64_t srow = sg.src_by_tok ? (int64_t)tk : row;
+        kr[k] = __ldg(reinterpret_cast<const uint4*>(ks + srow * src_row_stride) + w);
+        vr[k] = __ldg(reinterpret_cast<const uint4*>(vs + srow * src_row_stride) + w);
+        const int j0 = (w % cph) * 4;  // first pair of this chunk within the head
+        const float4* t = table + (pos * half + j0) / 2;
+        c0[k] = __ldg(t);
+        c1[k] = __ldg(t + 1);
+        dst[k] = pos * cache_row_stride + (int64_t)w * 8;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      if (dst[k] >= 0) {
+        *reinterpret_cast<uint4*>(kc + dst[k]) = rot8_bf16(kr[k], c0[k], c1[k]);
+        *reinterpret_cast<uint4*>(vc + dst[k]) = vr[k];
+      }
+    }
+  }
+}
+
+// Hot-path QKV epilogue for bf16 in/out, adjacent pairing: 16-B chunks of the
+// qkv row; q chunks -> q_out (rotated), k -> cache (rotated) + optional raw
+// copy, v -> cache.
+template <int UNR>
+__global__ void __launch_bounds__(256)
+qkv_bf16_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld_qkv,
+                const int32_t* __restrict__ positions, int64_t A, int Hq, int Hkv, int D,
+                const float4* __restrict__ table, __nv_bfloat16* __restrict__ q_out,
+                __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+                int64_t crs, __nv_bfloat16* __restrict__ k_raw) {
+  const int cph = D / 8;
+  const int upr = (Hq + 2 * Hkv) * cph;
+  const int half = D / 2;
+  const int64_t total = A * upr;
+  const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t u0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u0 < total;
+       u0 += nthr * UNR) {
+    uint4 x[UNR];
+    float4 c0[UNR], c1[UNR];
+    int64_t a_[UNR], pos_[UNR];
+    int w_[UNR];
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      const int64_t u = u0 + k * nthr;
+      a_[k] = -1;
+      if (u < total) {
+        const int64_t a = u / upr;
+        const int w = (int)(u - a * upr);
+        const int64_t pos = __ldg(positions + a);
+        x[k] = __ldg(reinterpret_cast<const uint4*>(qkv + a * ld_qkv) + w);
+        if (w < (Hq + Hkv) * cph) {
+          const int j0 = (w % cph) * 4;
+          const float4* t = table + (pos * half + j0) / 2;
+          c0[k] = __ldg(t);
+          c1[k] = __ldg(t + 1);
+        }
+        a_[k] = a;
+        pos_[k] = pos;
+        w_[k] = w;
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < UNR; ++k) {
+      if (a_[k] < 0) continue;
+      const int w = w_[k];
+      const int hh = w / cph, c = w % cph;
+      if (hh >= Hq + Hkv) {
+        *reinterpret_cast<uint4*>(vc + pos_[k] * crs + (int64_t)(hh - Hq - Hkv) * D + c * 8) = x[k];
+        continue;
+      }
+      const uint4 r = rot8_bf16(x[k], c0[k], c1[k]);
+      if (hh < Hq) {
+        *reinterpret_cast<uint4*>(q_out + (a_[k] * Hq + hh) * (int64_t)D + c * 8) = r;
+      } else {
+        *reinterpret_cast<uint4*>(kc + pos_[k] * crs + (int64_t)(hh - Hq) * D + c * 8) = r;
+        if (k_raw)
+          *reinterpret_cast<uint4*>(k_raw + (a_[k] * Hkv + hh - Hq) * (int64_t)D + c * 8) = x[k];
+      }
+    }
+  }
+}
+
 // grid: x = row blocks, y = segment.  256 threads; units per row = H*(D/2)/VEC.
 template <typename T, int VEC>
 __global__ void __launch_bounds__(256)
@@ -339,6 +461,25 @@ extern "C" int ct_gather_rope_blend(const ct_segment* segs, int n_segs, int64_t 
   }
   if (max_rows == 0) return CT_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  bool fast = dtype == CT_BF16 && pairing == CT_ROPE_ADJACENT && D % 8 == 0 &&
+              src_row_stride % 8 == 0 && cache_row_stride % 8 == 0 &&
+              ((uintptr_t)k_cache % 16 == 0) && ((uintptr_t)v_cache % 16 == 0) &&
+              ((uintptr_t)table % 16 == 0);
+  for (int i = 0; i < n_segs && fast; ++i)
+    fast = ((uintptr_t)segs[i].k % 16 == 0) && ((uintptr_t)segs[i].v % 16 == 0);
+  if (fast) {
+    constexpr int UNR = 4;
+    const int upr = (int)(H * D / 8);
+    int64_t bx = (max_rows * upr + 256 * UNR - 1) / (256 * UNR);
+    const int64_t cap = (148 * 8 + n_segs - 1) / n_segs;
+    if (bx > cap) bx = cap;
+    dim3 grid((unsigned)bx, (unsigned)n_segs);
+    blend_bf16_kernel<UNR><<<grid, 256, 0, st>>>(arr, src_row_stride, upr, (int)(D / 8),
+                                                 (const float4*)table, (int)(D / 2),
+                                                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache,
+                                                 cache_row_stride);
+    return check_launch("blend_bf16_kernel");
+  }
   const bool v4 = (D / 2) % 4 == 0;
   const int64_t upr = H * (D / 2) / (v4 ? 4 : 1);
   int64_t bx = (max_rows * upr + 255) / 256;
@@ -376,6 +517,21 @@ extern "C" int ct_qkv_rope_scatter(const void* qkv, int64_t ld_qkv, int in_dtype
     return fail(CT_ERR_PARAM, "dtype");
   if (A == 0) return CT_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (in_dtype == CT_BF16 && q_dtype == CT_BF16 && cache_dtype == CT_BF16 &&
+      pairing == CT_ROPE_ADJACENT && D % 8 == 0 && ld_qkv % 8 == 0 &&
+      cache_row_stride % 8 == 0 &&
+      (((uintptr_t)qkv | (uintptr_t)q_out | (uintptr_t)k_cache | (uintptr_t)v_cache |
+        (uintptr_t)table | (uintptr_t)k_raw_out) % 16 == 0)) {
+    constexpr int UNR = 4;
+    const int64_t units = A * (Hq + 2 * Hkv) * (D / 8);
+    int64_t g = (units + 256 * UNR - 1) / (256 * UNR);
+    if (g > 148 * 16) g = 148 * 16;
+    qkv_bf16_kernel<UNR><<<(unsigned)g, 256, 0, st>>>(
+        (const __nv_bfloat16*)qkv, ld_qkv, positions, A, (int)Hq, (int)Hkv, (int)D,
+        (const float4*)table, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
+        (__nv_bfloat16*)v_cache, cache_row_stride, (__nv_bfloat16*)k_raw_out);
+    return check_launch("qkv_bf16_kernel");
+  }
   const bool v4 = (D / 2) % 4 == 0;
   const int64_t units = A * (Hq + 2 * Hkv) * (D / 2) / (v4 ? 4 : 1);
   const unsigned g = grid_for(units, 256);
