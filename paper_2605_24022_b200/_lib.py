@@ -132,9 +132,18 @@ LAUNCH_COUNT = {"n": 0}
 _NOT_KERNELS = {"ct_copy_ranges_h2d", "ct_host_alloc", "ct_host_free"}
 
 
+_DEBUG_SYNC = bool(int(__import__("os").environ.get("CT_DEBUG_SYNC", "0")))
+
+
 def check(status: int, what: str = "") -> None:
     if what not in _NOT_KERNELS:
         LAUNCH_COUNT["n"] += 1
+    if _DEBUG_SYNC and status == 0:
+        import torch
+        try:
+            torch.cuda.synchronize()
+        except Exception as e:  # attribute the failure to this entry point
+            raise CudaError(f"{what}: {e}") from e
     if status != 0:
         cls = _STATUS.get(status, CacheTuneError)
         raise cls(f"{what}: {last_error()}" if what else last_error())

@@ -28,8 +28,8 @@ constexpr int TILE_M = 128;   // TMEM lanes / MMA M
 constexpr int BLK_N = 128;    // keys per block
 constexpr int HD = 128;       // head dim
 constexpr int KV_SLOTS = 5;
-constexpr int MAX_SPLIT = 4;
-constexpr int NSB = 3;               // S/P TMEM buffers        // softmax threads per tile row (key-column split)
+constexpr int MAX_SPLIT = 4;         // softmax threads per tile row (key-column split)
+constexpr int NSB = 3;               // S/P TMEM buffers
 constexpr int ATOM_BYTES = 128 * 64 * 2;      // [128 rows][64 bf16] swizzle-128B half tile
 constexpr int TILE_BYTES = 2 * ATOM_BYTES;    // 32 KiB: 128 rows x 128 bf16
 constexpr float LAZY_THRESH = 8.0f;           // log2 units
@@ -39,7 +39,9 @@ struct Smem {
   static constexpr int Q = 0;
   static constexpr int KV = Q + TILE_BYTES;
   static constexpr int BAR = KV + KV_SLOTS * TILE_BYTES;
-  static constexpr int NBAR = 1 + 2 * KV_SLOTS + 8;
+  // q + KV full/empty + per S/P buffer (S full, P full, PV done); the
+  // exchange area must not overlap the last barrier
+  static constexpr int NBAR = 1 + 2 * KV_SLOTS + 3 * 3;
   static constexpr int XCH = BAR + NBAR * 8;  // [3][MAX_SPLIT][128] f32 max/sum exchange
   static constexpr int TMEM_PTR = XCH + 3 * MAX_SPLIT * 128 * 4;
   static constexpr int TOTAL = TMEM_PTR + 16;
@@ -405,6 +407,9 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
     for (int j = 0; j < nb; ++j) {
       const int b = j % NSB;
       mbar_wait(bar_sfull(b), (j / NSB) & 1);
+      // lanes leave the try_wait spin independently: reconverge before the
+      // warp-collective (.sync.aligned) tcgen05.ld
+      __syncwarp();
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS(b) + lane_off + c * 32, r + c * 32);
@@ -486,6 +491,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         l = l * corr + ((s0 + s1) + (s2 + s3));  // partial row sum over this half
       }
       // P_j -> TMEM columns [hf*HALF/2, +HALF/2) of P buffer b (lane m)
+      __syncwarp();
 #pragma unroll
       for (int c = 0; c < HALF / 64; ++c) tmem_st32(tS(b) + lane_off_p + c * 32, pk + c * 32);
       if constexpr (HALF / 2 < 32) tmem_st16(tS(b) + lane_off_p, pk);
@@ -495,6 +501,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         // buffer (j-1)%3's barrier cannot alias: its previous phase (PV_{j-4})
         // completed before S_j was issued into buffer j%3 (in-order pipe).
         mbar_wait(bar_pvdone((j - 1) % NSB), ((j - 1) / NSB) & 1);
+        __syncwarp();  // reconverge before tcgen05.ld/st (.sync.aligned)
         tc_fence_after();
 #pragma unroll 1
         for (int c = 0; c < HALF / 32; ++c) {
@@ -521,6 +528,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       l = lt;
     }
     mbar_wait(bar_pvdone((nb - 1) % NSB), ((nb - 1) / NSB) & 1);  // PV_{nb-1} done
+    __syncwarp();
     tc_fence_after();
     const float inv = valid ? 1.f / l : 0.f;
     const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD + hf * HALF;

@@ -85,7 +85,7 @@ class SelectivePrefillEngine:
         self.caches = [(self.cache[l, 0], self.cache[l, 1]) for l in range(L)]
         self.buffers = LayerBuffers(model, self.A, dev)
         self.positions = torch.empty(self.A, dtype=torch.int32, device=dev)
-        self.tokens = torch.empty(self.A, dtype=torch.int32, device=dev)
+        self.tokens = torch.zeros(self.A, dtype=torch.int32, device=dev)  # suffix defaults to id 0
         self.positions[self.n_rec:] = torch.arange(self.history, self.n_ctx, dtype=torch.int32,
                                                    device=dev)
         self.keep = torch.empty(C * self.n_keep, dtype=torch.int32, device=dev)
