@@ -128,6 +128,47 @@ class SelectivePrefillEngine:
             self.segs.append((_lib.Segment * max(len(segs), 1))(*segs) if segs else None)
         self.n_segs = C if self.n_keep else 0
         self.launches_per_step = None
+        self.record_timeline = False
+        self._events: dict = {}
+
+    # real three-stream timeline (ct/pipesim.py Timeline schema) ------------------
+    def _ev(self, stream: str, layer: int, edge: int) -> torch.cuda.Event:
+        key = (stream, layer, edge)
+        ev = self._events.get(key)
+        if ev is None:
+            ev = torch.cuda.Event(enable_timing=True)
+            self._events[key] = ev
+        return ev
+
+    def _hook(self, l: int, phase: str) -> None:
+        # recompute l = QKV projection + RoPE/scatter of the selected rows;
+        # forward l = blend (waits on transfer l) + attention + projections/MLP
+        if phase == "start":
+            self._ev("recompute", l, 0).record()
+        elif phase == "recomputed":
+            self._ev("recompute", l, 1).record()
+            if not self.pinned or self.n_segs == 0:
+                self._ev("forward", l, 0).record()
+        else:
+            self._ev("forward", l, 1).record()
+
+    def timeline(self):
+        """Timeline of the last step recorded with record_timeline=True, in
+        seconds from the step start (ct/pipesim.py:93-105 schema); audit it
+        with pipesim.validate_timeline."""
+        from .pipesim import Timeline, TimelineEvent
+        t0 = self._ev("step", 0, 0)
+        events = []
+        for l in range(self.pool.L):
+            for stream, label in (("transfer", "gather" if l == 0 else "prefetch"),
+                                  ("recompute", "recompute+rope"),
+                                  ("forward", "fuse")):
+                if (stream, l, 0) not in self._events:
+                    continue
+                s = t0.elapsed_time(self._ev(stream, l, 0)) * 1e-3
+                e = t0.elapsed_time(self._ev(stream, l, 1)) * 1e-3
+                events.append(TimelineEvent(stream, l, s, e, label))
+        return Timeline(tuple(events), max(e.end_s for e in events))
 
     # algorithmic work per request -------------------------------------------------
     def attention_flops_per_layer(self) -> float:
@@ -145,6 +186,8 @@ class SelectivePrefillEngine:
         st = _dev.stream_handle()
         if self.pinned:
             torch.cuda.current_stream().wait_event(self.copy_done[l])
+            if self.record_timeline:
+                self._ev("forward", l, 0).record()   # fusion starts once transfer l landed
         t = self.timer.start("blend")
         pool = self.pool
         _lib.call("ct_gather_rope_blend", self.segs[l], self.n_segs, 2 * self.row_elems,
@@ -157,6 +200,8 @@ class SelectivePrefillEngine:
         """One request: suffix (host pinned or device int32 [S]) -> last-row logits."""
         pool, st = self.pool, _dev.stream_handle()
         C, N = pool.C, pool.N
+        if self.record_timeline:
+            self._ev("step", 0, 0).record()
         if self.pinned:
             self.step_start.record()
             with torch.cuda.stream(self.copy_stream):
@@ -164,8 +209,12 @@ class SelectivePrefillEngine:
                 cs = _dev.stream_handle(self.copy_stream)
                 for l in range(pool.L):
                     d, s, b = self.copy_args[l]
+                    if self.record_timeline:
+                        self._ev("transfer", l, 0).record(self.copy_stream)
                     _lib.call("ct_copy_ranges_h2d", d, s, b, C, cs)
                     self.copy_done[l].record(self.copy_stream)
+                    if self.record_timeline:
+                        self._ev("transfer", l, 1).record(self.copy_stream)
         if suffix is not None and self.S:
             self.tokens[self.n_rec:].copy_(suffix, non_blocking=True)
         m = self.meta
@@ -178,7 +227,8 @@ class SelectivePrefillEngine:
                       self.n_rec, 4, _dev.ptr(self.tokens), st)
         logits, _ = run_layers(self.model, self.tokens, self.positions, self.n_ctx, self.caches,
                                reuse=self._reuse, logits_rows="last", buffers=self.buffers,
-                               timer=self.timer)
+                               timer=self.timer,
+                               hook=self._hook if self.record_timeline else None)
         if logits_out is not None:
             logits_out.copy_(logits, non_blocking=True)
         return logits

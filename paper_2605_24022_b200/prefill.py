@@ -129,7 +129,7 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
                caches: Sequence, reuse: Callable[[int], None] | None = None,
                record_attention: bool = False, logits_rows: str | None = "all",
                k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None,
-               timer=None):
+               timer=None, hook: Callable[[int, str], None] | None = None):
     """Shared forward engine (ct/toymodel.py:135-193) over device inputs.
 
     tokens/positions: int32 [A] device.  caches[l] = (K, V) [n_ctx, Hkv, D]
@@ -156,12 +156,16 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
     probs_all = []
     for l, w in enumerate(model.layers):
         kc, vc = caches[l]
+        if hook is not None:
+            hook(l, "start")
         torch.mm(buf.x, w["wqkv"], out=buf.qkv)
         _lib.check(lib.ct_qkv_rope_scatter(
             _dev.ptr(buf.qkv), buf.qkv.shape[1], dtc, _dev.ptr(positions), a, hq, hkv, d,
             params.pairing_code, _dev.ptr(table), _dev.ptr(buf.q), dtc, _dev.ptr(kc),
             _dev.ptr(vc), dtc, hkv * d, _dev.ptr(k_raw_out[l]) if k_raw_out else None, st),
             "ct_qkv_rope_scatter")
+        if hook is not None:
+            hook(l, "recomputed")
         if reuse is not None:
             reuse(l)
         probs = (torch.empty((hq, a, n_ctx), dtype=torch.float32, device=dev)
@@ -189,6 +193,8 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
             dlt = _mm_f32(buf.act, down)
             _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), _dev.ptr(dlt), _lib.CT_F32, a,
                       hid, NORM_EPS, _dev.ptr(buf.x), dtc, st)
+        if hook is not None:
+            hook(l, "end")
     logits = None
     if logits_rows is not None and a:
         hrows = buf.h if logits_rows == "all" else buf.h[-1:]

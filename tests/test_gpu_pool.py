@@ -1,0 +1,97 @@
+"""Importance-ordered pool: sparse plan/fetch byte accounting and bit-exact rows
+against the reference's plans (tests/golden/pool_cases.npz), plus the serving
+engine's HBM vs pinned-host paths agreeing bit for bit."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ct():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2605_24022_b200 as ct
+    return ct
+
+
+@pytest.mark.parametrize("location", ["hbm", "pinned"])
+def test_pool_plans_match_reference_accounting(ct, location):
+    from paper_2605_24022_b200.pool import KvPool
+    g = golden("pool_cases")
+    for i in range(int(g["count"])):
+        layers, n, h, d, layer = (int(x) for x in g[f"p{i}_geom"])
+        r = float(g[f"p{i}_r"])
+        keys, vals = g[f"p{i}_keys"], g[f"p{i}_vals"]
+        chunk = ct.KvChunk(f"p{i}", tuple(ct.SeqTensor(k) for k in keys),
+                           tuple(ct.SeqTensor(v) for v in vals), source_tokens=np.arange(n))
+        rk = ct.rank_chunk(chunk)
+        dc = ct.DeviceChunk.from_host(chunk)
+        pool = KvPool([dc], [rk], location)
+        plan = pool.plan_sparse_fetch(f"p{i}", layer, r)
+        # same keep set and byte count as the reference's CTKV plan
+        assert np.array_equal(plan.keep_indices, g[f"p{i}_keep"])
+        assert plan.expected_bytes == int(g[f"p{i}_expected"])
+        # one contiguous range instead of the reference's coalesced runs
+        assert len(plan.byte_ranges) == (1 if plan.keep_count else 0)
+        before = pool.io_stats["bytes_read"]
+        K, V, keep = pool.fetch_sparse(plan)
+        if plan.keep_count:
+            assert pool.io_stats["bytes_read"] - before == plan.expected_bytes
+            assert np.array_equal(K.cpu().numpy(), keys[layer][keep])
+            assert np.array_equal(V.cpu().numpy(), vals[layer][keep])
+
+
+def test_engine_hbm_and_pinned_pools_agree(ct):
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=1024, seed=5)
+    m = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(5)
+    chunks = [ct.encode_chunk_isolated(m, rng.integers(0, 1024, size=512), chunk_id=f"c{j}")
+              for j in range(3)]
+    ranks = ct.rank_chunks(chunks)
+    suffix = torch.as_tensor(rng.integers(0, 1024, size=16).astype(np.int32), device="cuda")
+    outs = []
+    for loc in ("hbm", "pinned"):
+        eng = SelectivePrefillEngine(m, KvPool(chunks, ranks, loc), 0.15, 16)
+        outs.append(eng.step(suffix).float().cpu())
+        caches = eng.cache.float().cpu()
+        outs.append(caches)
+    assert torch.equal(outs[0], outs[2])
+    assert torch.equal(outs[1], outs[3])
+    # and the drop-in selective_prefill on the same inputs gives the same logits
+    ref = ct.selective_prefill(m, chunks, ranks, suffix.cpu().numpy(), 0.15, logits_rows="last")
+    assert torch.equal(ref.logits.float().cpu(), outs[0])
+
+
+def test_real_three_stream_timeline_audited(ct):
+    """CUDA-event timeline of a pinned-pool request in the simulator's schema
+    (ct/pipesim.py:93-105), checked with validate_timeline (ct/pipesim.py:257-279):
+    per-stream order, fusion after its transfer and recompute, and real overlap
+    of the PCIe transfer with the per-layer compute."""
+    from paper_2605_24022_b200 import pipesim
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    cfg = ct.ModelConfig.llama3_8b(n_layers=4, vocab_size=1024, seed=6)
+    m = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(6)
+    chunks = [ct.encode_chunk_isolated(m, rng.integers(0, 1024, size=2048), chunk_id=f"c{j}")
+              for j in range(4)]
+    ranks = ct.rank_chunks(chunks)
+    eng = SelectivePrefillEngine(m, KvPool(chunks, ranks, "pinned"), 0.15, 64)
+    eng.step()
+    eng.record_timeline = True
+    eng.step()
+    torch.cuda.synchronize()
+    tl = eng.timeline()
+    plan = pipesim.synthetic_plan([2048] * 4, 4, 0.15, 8, 128)
+    assert pipesim.validate_timeline(tl, plan) == []
+    csv = pipesim.timeline_to_csv(tl)
+    assert len(csv.splitlines()) == 1 + 3 * 4
+    busy = sum(e.end_s - e.start_s for e in tl.events)
+    assert busy > tl.ttft_s  # streams overlapped
