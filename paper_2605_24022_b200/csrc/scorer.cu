@@ -76,7 +76,7 @@ __device__ __forceinline__ void dft_small(cpx<T>* v) {
 template <typename T> struct ScoreCfg;
 // S complex signals (2S lanes) in flight per CTA; S*N*sizeof(cpx<T>) = 128 KiB.
 template <> struct ScoreCfg<double> { static constexpr int POINTS = 8192; };
-template <> struct ScoreCfg<float> { static constexpr int POINTS = 16384; };
+template <> struct ScoreCfg<float> { static constexpr int POINTS = 8192; };
 
 constexpr int SCORE_THREADS = 1024;
 constexpr int LANE_BLOCK = 128;
@@ -116,6 +116,14 @@ __device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
     if (b < total) {
       const int sg = b / NB, j = b % NB;
       const int jm = j % Ns;
+      // twiddles w^r by recurrence from one table load (fewer LSU ops; the
+      // extra complex multiplies run on the otherwise idle FP pipes)
+      cpx<T> w1 = {(T)1, (T)0};
+      if (jm > 0) {
+        w1 = tw[jm * step];
+        if (INV) w1.y = -w1.y;
+      }
+      cpx<T> wr = w1;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int idx = j + r * NB;
@@ -124,10 +132,9 @@ __device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
           const int kk = idx < N - idx ? idx : N - idx;
           if (kk >= cutoff) val = {(T)0, (T)0};
         }
-        if (r > 0 && jm > 0) {
-          cpx<T> w = tw[jm * r * step];
-          if (INV) w.y = -w.y;
-          val = cmul(val, w);
+        if (r > 0) {
+          val = cmul(val, wr);
+          wr = cmul(wr, w1);
         }
         v[k][r] = val;
       }

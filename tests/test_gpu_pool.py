@@ -65,7 +65,8 @@ def test_engine_hbm_and_pinned_pools_agree(ct):
     assert torch.equal(outs[0], outs[2])
     assert torch.equal(outs[1], outs[3])
     # and the drop-in selective_prefill on the same inputs gives the same logits
-    ref = ct.selective_prefill(m, chunks, ranks, suffix.cpu().numpy(), 0.15, logits_rows="last")
+    ref = ct.selective_prefill(m, chunks, ranks, suffix.cpu().numpy(), 0.15, logits_rows="last",
+                               record_attention=False)  # records force the SIMT path
     assert torch.equal(ref.logits.float().cpu(), outs[0])
 
 
