@@ -228,6 +228,43 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, uint32_t& o0, uint32_t& 
 // Which of a thread's 8 chunks of 8 scores take the FMA-pipe polynomial
 // instead of MUFU.ex2 (template parameter; 0 = all MUFU).
 
+// p = 2^(s*scale - m) for the thread's HALF scores: packed FFMA2 for the
+// argument, MUFU.ex2 or the polynomial per chunk (compile-time POLY), FADD2
+// row-sum accumulators, bf16x2 packing for the TMEM P store.
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b);
+
+template <int HALF, uint32_t POLY>
+__device__ __forceinline__ void softmax_chunks(const uint32_t* r, uint64_t sc2, uint64_t nm2,
+                                               uint64_t* acc2, uint32_t* pk) {
+#pragma unroll
+  for (int ch = 0; ch < HALF / 8; ++ch) {
+    uint64_t x2[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      x2[t] = ffma2(pk2(__uint_as_float(r[ch * 8 + 2 * t]), __uint_as_float(r[ch * 8 + 2 * t + 1])),
+                    sc2, nm2);
+    uint32_t e[8];
+    if (((POLY >> (ch & 31)) & 1) != 0) {  // folds per unrolled chunk
+#pragma unroll
+      for (int t = 0; t < 4; ++t) exp2_poly2(x2[t], e[2 * t], e[2 * t + 1]);
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        float x0, x1;
+        upk2(x2[t], x0, x1);
+        e[2 * t] = __float_as_uint(ex2(x0));
+        e[2 * t + 1] = __float_as_uint(ex2(x1));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e[2 * t] | ((uint64_t)e[2 * t + 1] << 32));
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+      pk[ch * 4 + t] = pack_bf16(__uint_as_float(e[2 * t]), __uint_as_float(e[2 * t + 1]));
+  }
+}
+
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -457,33 +494,11 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
       const uint64_t nm2 = pk2(-m_used, -m_used);
       uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
-#pragma unroll
-      for (int ch = 0; ch < HALF / 8; ++ch) {
-        uint64_t x2[4];
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          x2[t] = ffma2(pk2(__uint_as_float(r[ch * 8 + 2 * t]), __uint_as_float(r[ch * 8 + 2 * t + 1])),
-                        sc2, nm2);
-        uint32_t e[8];
-        if (((POLY_MASK >> ch) & 1) && !need_mask) {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) exp2_poly2(x2[t], e[2 * t], e[2 * t + 1]);
-        } else {
-#pragma unroll
-          for (int t = 0; t < 4; ++t) {
-            float x0, x1;
-            upk2(x2[t], x0, x1);
-            e[2 * t] = __float_as_uint(ex2(x0));
-            e[2 * t + 1] = __float_as_uint(ex2(x1));
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e[2 * t] | ((uint64_t)e[2 * t + 1] << 32));
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          pk[ch * 4 + t] = pack_bf16(__uint_as_float(e[2 * t]), __uint_as_float(e[2 * t + 1]));
-      }
+      // masked (diagonal) blocks take the all-MUFU path: -inf must give 0
+      if (need_mask)
+        softmax_chunks<HALF, 0u>(r, sc2, nm2, acc2, pk);
+      else
+        softmax_chunks<HALF, POLY_MASK>(r, sc2, nm2, acc2, pk);
       {
         float s0, s1, s2, s3;
         upk2(acc2[0], s0, s1);
@@ -648,7 +663,8 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   uint32_t poly = 0;
   if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
   auto kern = split == 4 ? attention_tc_kernel<4, 0> : split == 1 ? attention_tc_kernel<1, 0>
-            : poly == 0x22 ? attention_tc_kernel<2, 0x22> : attention_tc_kernel<2, 0>;
+            : poly == 0x22 ? attention_tc_kernel<2, 0x22> : poly == 0x01 ? attention_tc_kernel<2, 0x01>
+            : poly == 0x55 ? attention_tc_kernel<2, 0x55> : attention_tc_kernel<2, 0>;
   const int threads = 32 * (4 * (split == 4 ? 4 : split == 1 ? 1 : 2) + 2);
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const unsigned grid = (unsigned)(prm.n_qblocks * Hkv);

@@ -130,6 +130,7 @@ class SelectivePrefillEngine:
         self.launches_per_step = None
         self.record_timeline = False
         self._events: dict = {}
+        self.graph = None
 
     # real three-stream timeline (ct/pipesim.py Timeline schema) ------------------
     def _ev(self, stream: str, layer: int, edge: int) -> torch.cuda.Event:
@@ -232,6 +233,30 @@ class SelectivePrefillEngine:
         if logits_out is not None:
             logits_out.copy_(logits, non_blocking=True)
         return logits
+
+    # CUDA graph: one request (copies, selection, 32 layers, logits) replayed
+    # with a single launch instead of ~200 host launches ------------------------
+    def capture(self, suffix=None, logits_out: torch.Tensor | None = None) -> None:
+        """Capture step(suffix, logits_out) into a CUDA graph.  replay() re-runs
+        it reading the CURRENT contents of the same suffix/logits buffers."""
+        timing, self.timer.enabled = self.timer.enabled, False
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self.step(suffix, logits_out)          # warm-up: allocations, tables
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        n0 = _lib.LAUNCH_COUNT["n"]
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self._graph_logits = self.step(suffix, logits_out)
+        self.launches_per_step = _lib.LAUNCH_COUNT["n"] - n0
+        self.timer.enabled = timing
+
+    def replay(self) -> torch.Tensor:
+        self.graph.replay()
+        _lib.LAUNCH_COUNT["n"] += self.launches_per_step or 0
+        return self._graph_logits
 
 
 class FullPrefillEngine:
