@@ -262,8 +262,20 @@ def pool_cases(ct):
     np.savez_compressed(OUT / "pool_cases.npz", **out)
 
 
+def ctkv_cases(ct):
+    """Reference-written CTKV files (ranked and bare) for format parity."""
+    rng = np.random.default_rng(6161)
+    keys = [rng.standard_normal((32, 2, 8)).astype(np.float32) for _ in range(4)]
+    vals = [rng.standard_normal((32, 2, 8)).astype(np.float32) for _ in range(4)]
+    chunk = _chunk(ct, keys, vals, cid="fmt")
+    rk = ct.rank_chunk(chunk, 0.5)
+    (OUT / "fmt_ranked.ctkv").write_bytes(ct.write_ctkv(chunk, rk))
+    (OUT / "fmt_bare.ctkv").write_bytes(ct.write_ctkv(chunk))
+
+
 def main():
     ct = _ref()
+    ctkv_cases(ct)
     spectral_cases(ct)
     big_chunks(ct)
     rope_cases(ct)
