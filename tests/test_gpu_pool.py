@@ -96,3 +96,25 @@ def test_real_three_stream_timeline_audited(ct):
     assert len(csv.splitlines()) == 1 + 3 * 4
     busy = sum(e.end_s - e.start_s for e in tl.events)
     assert busy > tl.ttft_s  # streams overlapped
+
+
+def test_offline_prepare_pool_and_ctkv_export(ct, tmp_path):
+    """GPU offline stage: encode + rank + importance-ordered pool, CTKV export
+    readable by the reference format parser, rankings identical to rank_chunk."""
+    from paper_2605_24022_b200 import ctkv
+    from paper_2605_24022_b200.offline import prepare_pool
+    from oracle import cachetune_oracle as O
+    om = O.Model(O.ModelConfig(seed=2, n_layers=2))
+    rng = np.random.default_rng(9)
+    toks = [rng.integers(0, 256, size=256) for _ in range(3)]
+    timings = {}
+    pool = prepare_pool(om, toks, location="pinned", ctkv_dir=tmp_path, timings=timings)
+    assert set(timings) == {"encode_ms", "rank_ms", "pool_ms"}
+    for i in range(3):
+        chunk, rk = ctkv.read_ctkv((tmp_path / f"chunk{i}.ctkv").read_bytes(), f"chunk{i}")
+        assert np.array_equal(rk.aggregate_order, pool.agg[i].cpu().numpy())
+        again = ct.rank_chunk(chunk)
+        assert np.array_equal(again.aggregate_order, rk.aggregate_order)
+        # the exported chunk KV is the oracle's isolated encoding (fp32 mode)
+        kr, vs = O.encode_chunk_isolated(om, toks[i])
+        assert O.normwise_rel(chunk.keys_raw[1].data, kr[1]) < 1e-5
