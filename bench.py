@@ -337,7 +337,16 @@ def run_ours(args, rank, world, local_rank):
         del full
         torch.cuda.empty_cache()
 
-    # ---- aggregate over ranks (max of times), result gather off the hot path
+    # ---- result gather off the hot path (config 5: first-token logits,
+    # selected positions, TTFT of every rank's request to rank 0 over NCCL)
+    from paper_2605_24022_b200.distributed import RequestResult, gather_results
+    g0 = time.perf_counter()
+    gathered = gather_results(
+        [RequestResult(rank, statistics.median(step_ms), ref_logits[0].float(),
+                       eng.positions[:eng.n_rec].clone())], cfg.vocab_size, eng.n_rec, device=dev)
+    gather_ms = (time.perf_counter() - g0) * 1e3
+
+    # ---- aggregate over ranks (max of times)
     def allmax(x):
         if world == 1 or x is None:
             return x
@@ -411,6 +420,8 @@ def run_ours(args, rank, world, local_rank):
         "ttft_speedup_vs_full": (full_ms / p50) if full_ms else None,
         "flop_ratio_bound": (full_flops / step_flops) if full_flops else None,
         "gpu_launches": launches,
+        "result_gather": {"requests": len(gathered) if gathered else 0, "ms": gather_ms,
+                          "note": "all_gather of logits/selections/TTFT after the timed region"},
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
