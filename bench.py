@@ -64,6 +64,16 @@ def load_peaks():
     return dict(hbm=6650.0, bf16=1590.0, bf16_sust=1400.0, src="fallback (B200_PROFILING.md)")
 
 
+def ncu_traffic(kernel: str, config: str):
+    """DRAM bytes per launch from the committed ncu capture (profiles/ncu_traffic.json);
+    only meaningful for the config the capture was taken on (config 2)."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if config != "cfg2" or not p.exists():
+        return None
+    entry = json.loads(p.read_text()).get(kernel)
+    return None if entry is None else entry["bytes"]
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -400,13 +410,16 @@ def run_ours(args, rank, world, local_rank):
                    "active_rows": eng.A, "n_ctx": eng.n_ctx, "keep_rows_per_chunk": eng.n_keep},
         "roofline": {"kernel": "ct_selective_attention (tcgen05)", "bound": "tensor",
                      "achieved": att_tflops, "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
-                     "frac": att_tflops / peaks["bf16_sust"], "traffic": None,
+                     "frac": att_tflops / peaks["bf16_sust"],
+                     "traffic": ncu_traffic("attention_tc_kernel", args.config),
                      "flops_per_launch": att_flops, "launch_ms": att_ms,
                      "peak_source": peaks["src"] + " bf16 sustained"},
         "kernels": {
             "gather_rope_blend": {"bound": "hbm", "achieved": blend_gbs, "peak": peaks["hbm"],
                                   "unit": "GB/s", "frac": blend_gbs / peaks["hbm"],
-                                  "bytes_per_launch": blend_bytes, "launch_ms": blend_ms},
+                                  "bytes_per_launch": blend_bytes, "launch_ms": blend_ms,
+                                  "traffic": ncu_traffic("gather_rope_blend_kernel",
+                                                         args.config)},
             "scorer_f64_per_request": {"ms": sc64, "bytes": scorer_bytes,
                                        "hbm_gbs": scorer_bytes / (sc64 * 1e-3) / 1e9},
             "scorer_f32_per_request": {"ms": sc32,
