@@ -76,6 +76,18 @@ int ct_score_chunks(const void* keys, const void* values, int dtype,
                     int32_t* layer_order, int32_t* agg_order,
                     void* workspace, size_t workspace_bytes, void* stream);
 
+/* Same as ct_score_chunks with a band selector: band 0 = the low band above,
+ * band 1 = the complementary high band (min(k, N-k) >= cutoff), the score the
+ * reference's "highfreq" selection strategy uses
+ * (ct/toymodel.py:355-358 -> ct/spectral.py high_freq_scores). */
+int ct_score_chunks_band(const void* keys, const void* values, int dtype,
+                         int64_t C, int64_t L, int64_t N, int64_t lanes,
+                         int64_t ld_token, int64_t ld_layer, int64_t ld_chunk,
+                         int64_t cutoff, int precision, int band,
+                         double* layer_scores, double* agg_scores,
+                         int32_t* layer_order, int32_t* agg_order,
+                         void* workspace, size_t workspace_bytes, void* stream);
+
 /* Stable descending argsort of `rows` rows of n f64 scores (ties -> lower
  * index): ct/spectral.py:99-101.  order is int32 [rows][n]. */
 int ct_desc_order(const double* scores, int64_t rows, int64_t n,

@@ -49,12 +49,13 @@ def cutoff_index(alpha: float, n_freqs: int) -> int:
 
 
 def low_freq_scores(keys: np.ndarray, values: np.ndarray,
-                    alpha: float = 0.5) -> np.ndarray:
+                    alpha: float = 0.5, band: str = "low") -> np.ndarray:
     """ct/spectral.py:69-90 (_band_scores, band='low').
 
     keys/values: [N, H, D] float32 (token-major).  For each tensor: float64
-    rfft along tokens, zero bins >= c, irfft(n=N), per-token L2 norm over the
-    flattened H*D row; score = 0 + 0.5*|K~_i| + 0.5*|V~_i|.
+    rfft along tokens, zero bins >= c (band='high': bins < c, ct/spectral.py:47-54),
+    irfft(n=N), per-token L2 norm over the flattened H*D row;
+    score = 0 + 0.5*|K~_i| + 0.5*|V~_i|.
     """
     if keys.shape != values.shape:
         raise ValueError("shape mismatch")
@@ -65,10 +66,18 @@ def low_freq_scores(keys: np.ndarray, values: np.ndarray,
     for t in (keys, values):
         spec = np.fft.rfft(np.asarray(t, dtype=np.float32).astype(np.float64), axis=0)
         c = cutoff_index(alpha, spec.shape[0])
-        spec[c:] = 0.0
+        if band == "low":
+            spec[c:] = 0.0
+        else:
+            spec[:c] = 0.0
         recon = np.fft.irfft(spec, n=n, axis=0)
         out += 0.5 * np.linalg.norm(recon.reshape(n, -1), axis=1)
     return out
+
+
+def high_freq_scores(keys: np.ndarray, values: np.ndarray, alpha: float = 0.5) -> np.ndarray:
+    """ct/spectral.py:93-96 -- the complementary high band."""
+    return low_freq_scores(keys, values, alpha, band="high")
 
 
 def descending_order(scores: np.ndarray) -> np.ndarray:

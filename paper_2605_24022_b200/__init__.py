@@ -16,7 +16,8 @@ __version__ = "0.1.0"
 
 _LAZY = {
     "ImportanceRanking": "spectral", "rank_chunk": "spectral", "rank_chunks": "spectral",
-    "low_freq_scores": "spectral", "indices_for_ratio": "spectral",
+    "low_freq_scores": "spectral", "high_freq_scores": "spectral",
+    "indices_for_ratio": "spectral",
     "complement_for_ratio": "spectral", "selection_count": "spectral",
     "cutoff_index": "spectral", "score_device": "spectral", "select_device": "spectral",
     "RopeParams": "rope", "rope_apply": "rope",
@@ -25,6 +26,8 @@ _LAZY = {
     "selective_prefill": "prefill", "full_prefill": "prefill",
     "encode_chunk_isolated": "prefill", "PrefillResult": "prefill",
     "AttentionRecord": "prefill", "attention_deviation": "prefill",
+    "STRATEGIES": "experiments", "strategy_ranking": "experiments",
+    "effective_ratio": "experiments", "run_selection_experiment": "experiments",
 }
 
 

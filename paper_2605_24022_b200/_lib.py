@@ -57,6 +57,10 @@ _SIGS = {
     "ct_score_chunks": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
                                 c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p,
                                 c_void_p, c_void_p, c_void_p, c_size_t, c_void_p]),
+    "ct_score_chunks_band": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64,
+                                     c_int64, c_int64, c_int64, c_int64, c_int64, c_int, c_int,
+                                     c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
+                                     c_void_p]),
     "ct_desc_order": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ct_selection_plan": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
                                   c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),

@@ -130,7 +130,8 @@ __device__ __forceinline__ void stockham_pass(cpx<T>* sig, int S, int Ns,
         cpx<T> val = sig[spad(sg * N + idx)];
         if (MASK) {
           const int kk = idx < N - idx ? idx : N - idx;
-          if (kk >= cutoff) val = {(T)0, (T)0};
+          // cutoff >= 0: low band keeps min(k,N-k) < c; cutoff = -(c+1): high band
+          if (cutoff >= 0 ? kk >= cutoff : kk < -cutoff - 1) val = {(T)0, (T)0};
         }
         if (r > 0) {
           val = cmul(val, wr);
@@ -269,20 +270,24 @@ fft_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
   }
 }
 
-// Circulant low-pass kernel p[m] = (1/N)(1 + 2 sum_{k=1}^{kmax} cos(2 pi k m/N)
-// + nyq (-1)^m): the exact impulse response of rfft -> zero bins >= c -> irfft.
+// Circulant band kernel p[m] = (1/N) sum_{k in band} w_k cos(2 pi k m/N) over
+// rfft bins k in [0, N/2] (w_k = 1 for DC and an even-N Nyquist bin, else 2):
+// the exact impulse response of rfft -> zero the other bins -> irfft.  Low band
+// (cutoff = c >= 0) keeps k < c; cutoff = -(c+1) keeps the high band k >= c.
+// An empty band sums nothing, so its scores are exactly 0 like the reference's.
 __global__ void lowpass_kernel_table(int N, int cutoff, double* p) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= N) return;
-  if (cutoff <= 0) { p[m] = 0.0; return; }
-  const int kmax = min(cutoff - 1, (N - 1) / 2);
-  const bool nyq = (N % 2 == 0) && (cutoff >= N / 2 + 1);
-  double s = 1.0;
-  for (int k = 1; k <= kmax; ++k) {
+  const bool high = cutoff < 0;
+  const int c = high ? -cutoff - 1 : cutoff;
+  const int klo = high ? c : 0;
+  const int khi = high ? N / 2 : min(c - 1, N / 2);
+  double s = 0.0;
+  for (int k = klo; k <= khi; ++k) {
     const long long km = ((long long)k * m) % N;
-    s += 2.0 * cospi(2.0 * (double)km / (double)N);
+    const double w = (k == 0 || 2 * k == N) ? 1.0 : 2.0;
+    s += w * cospi(2.0 * (double)km / (double)N);
   }
-  if (nyq) s += (m & 1) ? -1.0 : 1.0;
   p[m] = s / (double)N;
 }
 
@@ -542,7 +547,20 @@ extern "C" int ct_score_chunks(const void* keys, const void* values, int dtype, 
                                double* layer_scores, double* agg_scores, int32_t* layer_order,
                                int32_t* agg_order, void* workspace, size_t workspace_bytes,
                                void* stream) {
+  return ct_score_chunks_band(keys, values, dtype, C, L, N, lanes, ld_token, ld_layer, ld_chunk,
+                              cutoff, precision, 0, layer_scores, agg_scores, layer_order,
+                              agg_order, workspace, workspace_bytes, stream);
+}
+
+extern "C" int ct_score_chunks_band(const void* keys, const void* values, int dtype, int64_t C,
+                                    int64_t L, int64_t N, int64_t lanes, int64_t ld_token,
+                                    int64_t ld_layer, int64_t ld_chunk, int64_t cutoff,
+                                    int precision, int band, double* layer_scores,
+                                    double* agg_scores, int32_t* layer_order,
+                                    int32_t* agg_order, void* workspace, size_t workspace_bytes,
+                                    void* stream) {
   cudaStream_t st = (cudaStream_t)stream;
+  if (band != 0 && band != 1) return fail(CT_ERR_PARAM, "band %d", band);
   if (C < 1 || L < 1 || N < 1 || lanes < 1)
     return fail(CT_ERR_SHAPE, "score geometry C=%lld L=%lld N=%lld lanes=%lld", (long long)C,
                 (long long)L, (long long)N, (long long)lanes);
@@ -551,6 +569,7 @@ extern "C" int ct_score_chunks(const void* keys, const void* values, int dtype, 
   if (cutoff < 0 || cutoff > N / 2 + 1) return fail(CT_ERR_PARAM, "cutoff %lld", (long long)cutoff);
   if (!keys || !values || !layer_scores) return fail(CT_ERR_PARAM, "null tensor");
   if (C * L > 65535) return fail(CT_ERR_UNSUPPORTED, "C*L too large");
+  const int cut = band ? -(int)(cutoff + 1) : (int)cutoff;  // kernels: <0 = high band
   if (workspace_bytes < ct_score_workspace_bytes(C, L, N, lanes, precision))
     return fail(CT_ERR_PARAM, "workspace too small");
   const int nlb = (int)((lanes + LANE_BLOCK - 1) / LANE_BLOCK);
@@ -569,22 +588,22 @@ extern "C" int ct_score_chunks(const void* keys, const void* values, int dtype, 
     if (precision == CT_F64) {
       rc = dtype == CT_F32
                ? launch_fft<double, float>(lg, keys, values, (int)L, (int)C, (int)lanes, ld_token,
-                                           ld_layer, ld_chunk, (int)cutoff, tw_d, partial, st)
+                                           ld_layer, ld_chunk, cut, tw_d, partial, st)
                : launch_fft<double, __nv_bfloat16>(lg, keys, values, (int)L, (int)C, (int)lanes,
-                                                   ld_token, ld_layer, ld_chunk, (int)cutoff, tw_d,
+                                                   ld_token, ld_layer, ld_chunk, cut, tw_d,
                                                    partial, st);
     } else {
       rc = dtype == CT_F32
                ? launch_fft<float, float>(lg, keys, values, (int)L, (int)C, (int)lanes, ld_token,
-                                          ld_layer, ld_chunk, (int)cutoff, tw_f, partial, st)
+                                          ld_layer, ld_chunk, cut, tw_f, partial, st)
                : launch_fft<float, __nv_bfloat16>(lg, keys, values, (int)L, (int)C, (int)lanes,
-                                                  ld_token, ld_layer, ld_chunk, (int)cutoff, tw_f,
+                                                  ld_token, ld_layer, ld_chunk, cut, tw_f,
                                                   partial, st);
     }
     if (rc) return rc;
   } else {
     double* p = (double*)tw_d;
-    lowpass_kernel_table<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((int)N, (int)cutoff, p);
+    lowpass_kernel_table<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((int)N, cut, p);
     if ((rc = check_launch("lowpass_kernel_table"))) return rc;
     dim3 grid((unsigned)((N + 31) / 32), (unsigned)(2 * nlb), (unsigned)(C * L));
     if (dtype == CT_F32)

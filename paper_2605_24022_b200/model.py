@@ -127,6 +127,30 @@ class GpuModel:
                               dtype=dtype, device=device)
 
     @classmethod
+    def reference_init(cls, config: ModelConfig, dtype=torch.float32, device="cuda"):
+        """The reference ToyModel's seeded weights (ct/toymodel.py:61-79): the same
+        numpy default_rng(seed) draw order, so a seed names the same model here as
+        in the reference's experiments.  Reference geometry only (MHA, relu MLP)."""
+        if config.kv_heads != config.n_heads or config.mlp_kind not in (None, "relu"):
+            raise ShapeError("reference_init covers the reference ToyModel geometry only")
+        hid = config.hidden_dim
+        rng = np.random.default_rng(config.seed)
+        scale = 1.0 / np.sqrt(hid)
+
+        def w(*shape):
+            return rng.uniform(-1.0, 1.0, size=shape) * scale
+        emb = w(config.vocab_size, hid)
+        layers = []
+        for _ in range(config.n_layers):
+            layer = {"wq": w(hid, hid), "wk": w(hid, hid), "wv": w(hid, hid), "wo": w(hid, hid)}
+            if config.mlp_kind == "relu":
+                layer["w1"] = w(hid, 4 * hid)
+                layer["w2"] = w(4 * hid, hid)
+            layers.append(layer)
+        return cls.from_numpy(config, emb, layers, w(hid, config.vocab_size), dtype=dtype,
+                              device=device)
+
+    @classmethod
     def random(cls, config: ModelConfig, dtype=torch.bfloat16, device="cuda", seed=None):
         """U(-1,1)/sqrt(hid) weights drawn on the device (ct/toymodel.py:64-68 law)."""
         gen = torch.Generator(device=device)

@@ -97,7 +97,10 @@ def _as_device_kv(keys, values):
         if isinstance(x, torch.Tensor):
             return x.to(dev)
         data = x.data if hasattr(x, "data") and not isinstance(x, np.ndarray) else x
-        return torch.from_numpy(np.ascontiguousarray(np.asarray(data, dtype=np.float32))).to(dev)
+        arr = np.ascontiguousarray(np.asarray(data, dtype=np.float32))
+        if not arr.flags.writeable:  # SeqTensor data is frozen; torch wants writable
+            arr = arr.copy()
+        return torch.from_numpy(arr).to(dev)
     k, v = conv(keys), conv(values)
     if k.dim() == 3:
         k, v = k.unsqueeze(0), v.unsqueeze(0)
@@ -105,13 +108,15 @@ def _as_device_kv(keys, values):
 
 
 def score_device(keys: torch.Tensor, values: torch.Tensor, alpha: float = DEFAULT_ALPHA,
-                 precision: str = "f64", want_layer_order: bool = True):
-    """Score C chunks on the device.
+                 precision: str = "f64", want_layer_order: bool = True, band: str = "low"):
+    """Score C chunks on the device (band "low", or "high" = ct/spectral.py:47-54).
 
     keys/values: [C, L, N, H, D] (or [L, N, H, D]) f32/bf16 CUDA tensors.
     Returns dict of device tensors: layer_scores [C,L,N] f64, agg [C,N] f64,
     layer_order [C,L,N] int32 (optional), agg_order [C,N] int32."""
     _check_alpha(alpha)
+    if band not in ("low", "high"):
+        raise InvalidParam(f"band must be 'low' or 'high', got {band!r}")
     if keys.shape != values.shape:
         raise ShapeError(f"keys {tuple(keys.shape)} vs values {tuple(values.shape)}")
     if keys.dim() == 4:
@@ -134,11 +139,12 @@ def score_device(keys: torch.Tensor, values: torch.Tensor, alpha: float = DEFAUL
     lib = _lib.load()
     wsb = lib.ct_score_workspace_bytes(C, L, N, lanes, prec)
     ws = _dev.workspace(wsb, "score")
-    _lib.check(lib.ct_score_chunks(
+    _lib.check(lib.ct_score_chunks_band(
         _dev.ptr(keys), _dev.ptr(values), _dev.ct_dtype(keys.dtype), C, L, N, lanes,
-        lanes, N * lanes, L * N * lanes, cutoff, prec,
+        lanes, N * lanes, L * N * lanes, cutoff, prec, 1 if band == "high" else 0,
         _dev.ptr(out["layer_scores"]), _dev.ptr(out["agg"]), _dev.ptr(out["layer_order"]),
-        _dev.ptr(out["agg_order"]), _dev.ptr(ws), wsb, _dev.stream_handle()), "ct_score_chunks")
+        _dev.ptr(out["agg_order"]), _dev.ptr(ws), wsb, _dev.stream_handle()),
+        "ct_score_chunks_band")
     return out
 
 
@@ -155,6 +161,19 @@ def low_freq_scores(keys, values, alpha: float = DEFAULT_ALPHA,
     return out["layer_scores"][0, 0].cpu().numpy()
 
 
+def high_freq_scores(keys, values, alpha: float = DEFAULT_ALPHA,
+                     precision: str = "f64") -> np.ndarray:
+    """Mirror of low_freq_scores on the complementary high band (ct/spectral.py:93-96)."""
+    _check_alpha(alpha)
+    ks = getattr(keys, "shape", None)
+    vs = getattr(values, "shape", None)
+    if tuple(ks) != tuple(vs):
+        raise ShapeError(f"keys {ks} vs values {vs}")
+    k, v = _as_device_kv(keys, values)
+    out = score_device(k, v, alpha, precision, want_layer_order=False, band="high")
+    return out["layer_scores"][0, 0].cpu().numpy()
+
+
 def _chunk_tensors(chunk):
     if isinstance(chunk, DeviceChunk):
         return chunk.keys, chunk.values
@@ -164,11 +183,13 @@ def _chunk_tensors(chunk):
     return torch.from_numpy(k).to(dev), torch.from_numpy(v).to(dev)
 
 
-def rank_chunk(chunk, alpha: float = DEFAULT_ALPHA, precision: str = "f64") -> ImportanceRanking:
-    """Score every layer and build the importance permutations (ct/spectral.py:149-159)."""
+def rank_chunk(chunk, alpha: float = DEFAULT_ALPHA, precision: str = "f64",
+               band: str = "low") -> ImportanceRanking:
+    """Score every layer and build the importance permutations (ct/spectral.py:149-159;
+    band="high" is the highfreq strategy's ranking, ct/toymodel.py:356-363)."""
     _check_alpha(alpha)
     k, v = _chunk_tensors(chunk)
-    out = score_device(k, v, alpha, precision)
+    out = score_device(k, v, alpha, precision, band=band)
     n = k.shape[1]
     return ImportanceRanking(
         per_layer_scores=out["layer_scores"][0].cpu().numpy(),

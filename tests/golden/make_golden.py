@@ -273,8 +273,59 @@ def ctkv_cases(ct):
     (OUT / "fmt_bare.ctkv").write_bytes(ct.write_ctkv(chunk))
 
 
+def highband_cases(ct):
+    """high_freq_scores / the highfreq strategy ranking (ct/spectral.py:93-96,
+    ct/toymodel.py:356-363) over awkward geometries and cutoffs."""
+    from cachetune import toymodel
+    rng = np.random.default_rng(20261017)
+    geoms = [(1, 1, 2, 1), (7, 2, 4, 2), (16, 2, 4, 3), (33, 1, 8, 2), (64, 4, 8, 2),
+             (100, 2, 4, 2), (128, 2, 8, 2), (257, 1, 2, 2), (1024, 2, 4, 1), (96, 2, 64, 1)]
+    out = {}
+    i = 0
+    for (n, h, d, l) in geoms:
+        for alpha in (0.0, 0.3, 0.5, 1.0):
+            keys = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(l)]
+            vals = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(l)]
+            rk = toymodel.strategy_ranking(_chunk(ct, keys, vals), "highfreq", alpha)
+            out[f"c{i}_keys"] = np.stack(keys)
+            out[f"c{i}_vals"] = np.stack(vals)
+            out[f"c{i}_alpha"] = np.float64(alpha)
+            out[f"c{i}_scores"] = rk.per_layer_scores
+            out[f"c{i}_orders"] = np.asarray(rk.per_layer_order).astype(np.int32)
+            out[f"c{i}_agg"] = np.asarray(rk.aggregate_order).astype(np.int32)
+            i += 1
+    out["count"] = np.int64(i)
+    np.savez_compressed(OUT / "highband_cases.npz", **out)
+
+
+def experiment_cases(ct):
+    """Per-seed suffix-attention deviations of run_selection_experiment
+    (ct/toymodel.py:374-419) for every strategy on the acceptance suite's
+    committed seeds (pkg/tests/test_acceptance.py:28,187-201), plus the
+    reference's random-strategy permutations for seed 0."""
+    from cachetune import toymodel
+    seeds = list(range(25))
+    out = {"seeds": np.array(seeds)}
+    for strategy in toymodel.STRATEGIES:
+        res = toymodel.run_selection_experiment(seeds, r=0.15, strategy=strategy)
+        out[f"dev_{strategy}"] = np.array([d for _, d in res])
+    for strategy in ("lowfreq", "none"):
+        res = toymodel.run_selection_experiment([0, 1, 2], 0.25, strategy,
+                                                chunk_tokens=(24, 24), suffix_len=6)
+        out[f"small_{strategy}"] = np.array([d for _, d in res])
+    res = toymodel.run_selection_experiment([3, 4], r=0.3, strategy="lowfreq", mlp=True)
+    out["mlp_lowfreq"] = np.array([d for _, d in res])
+    np.savez_compressed(OUT / "experiment_cases.npz", **out)
+
+
 def main():
     ct = _ref()
+    if len(sys.argv) > 1:  # regenerate only the named fixtures
+        for name in sys.argv[1:]:
+            globals()[name](ct)
+        return
+    highband_cases(ct)
+    experiment_cases(ct)
     ctkv_cases(ct)
     spectral_cases(ct)
     big_chunks(ct)

@@ -51,6 +51,40 @@ def test_spectral_cases_bit_exact(ct):
             assert np.array_equal(ct.indices_for_ratio(rk, r), g[f"c{i}_{tag}"]), (i, r)
 
 
+def test_highband_cases_bit_exact(ct):
+    """Device high band (ct_score_chunks_band, band=1) vs the reference's
+    highfreq strategy ranking (ct/toymodel.py:356-363)."""
+    from paper_2605_24022_b200.experiments import strategy_ranking
+    g = golden("highband_cases")
+    for i in range(int(g["count"])):
+        keys, vals, alpha = g[f"c{i}_keys"], g[f"c{i}_vals"], float(g[f"c{i}_alpha"])
+        chunk = ct.KvChunk("c", tuple(ct.SeqTensor(k) for k in keys),
+                           tuple(ct.SeqTensor(v) for v in vals))
+        rk = strategy_ranking(chunk, "highfreq", alpha)
+        want = g[f"c{i}_scores"]
+        np.testing.assert_allclose(rk.per_layer_scores, want, rtol=1e-11,
+                                   atol=1e-13 * max(1.0, float(np.max(want))), err_msg=str(i))
+        assert np.array_equal(rk.aggregate_order, g[f"c{i}_agg"]), i
+        assert np.array_equal(rk.per_layer_order, g[f"c{i}_orders"]), i
+        hs = ct.high_freq_scores(ct.SeqTensor(keys[0]), ct.SeqTensor(vals[0]), alpha)
+        np.testing.assert_allclose(hs, want[0], rtol=1e-11,
+                                   atol=1e-13 * max(1.0, float(np.max(want))))
+
+
+def test_highband_big_chunk_complements_lowband(ct):
+    """High band at config-2 chunk length (the N=2048 Stockham path) vs the oracle."""
+    from oracle import cachetune_oracle as O
+    keys, vals = _big(11, (1, 2048, 8, 128))
+    k = torch.from_numpy(np.stack(keys)).cuda()
+    v = torch.from_numpy(np.stack(vals)).cuda()
+    from paper_2605_24022_b200.spectral import score_device
+    hi = score_device(k, v, 0.5, band="high")
+    want = O.high_freq_scores(keys[0], vals[0], 0.5)
+    got = hi["layer_scores"][0, 0].cpu().numpy()
+    np.testing.assert_allclose(got, want, rtol=1e-11, atol=1e-12 * float(want.max()))
+    assert np.array_equal(hi["agg_order"][0].cpu().numpy(), O.descending_order(want))
+
+
 def _big(seed, geom):
     l, n, h, d = geom
     rng = np.random.default_rng(seed)

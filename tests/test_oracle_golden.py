@@ -21,6 +21,18 @@ def test_spectral_cases_bit_exact():
             assert np.array_equal(O.indices_for_ratio(agg, r), g[f"c{i}_{tag}"]), (i, r)
 
 
+def test_highband_cases_bit_exact():
+    """Oracle high band vs the reference's highfreq strategy ranking."""
+    g = golden("highband_cases")
+    for i in range(int(g["count"])):
+        keys, vals, alpha = g[f"c{i}_keys"], g[f"c{i}_vals"], float(g[f"c{i}_alpha"])
+        scores = np.stack([O.high_freq_scores(k, v, alpha) for k, v in zip(keys, vals)])
+        np.testing.assert_allclose(scores, g[f"c{i}_scores"], rtol=1e-12, atol=1e-300)
+        assert np.array_equal(np.stack([O.descending_order(s) for s in scores]),
+                              g[f"c{i}_orders"]), i
+        assert np.array_equal(O.descending_order(scores.mean(axis=0)), g[f"c{i}_agg"]), i
+
+
 def test_big_chunk_regenerated_inputs_and_orders():
     g = golden("big_chunks")
     l, n, h, d = g["geometry"]
