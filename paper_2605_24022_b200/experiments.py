@@ -20,7 +20,9 @@ from typing import Sequence
 import numpy as np
 import torch
 
+from . import _dev
 from .errors import InvalidPlan
+from .kvcore import DeviceChunk
 from .model import GpuModel, ModelConfig
 from .prefill import attention_deviation, encode_chunk_isolated, full_prefill, selective_prefill
 from .spectral import ImportanceRanking, rank_chunk
@@ -84,3 +86,68 @@ def run_selection_experiment(seeds: Sequence[int], r: float = 0.15,
                                   sel.attention.suffix_view(history))
         results.append((seed, dev))
     return results
+
+
+def attention_recovery_at_scale(model: GpuModel, chunk_tokens: Sequence, suffix: Sequence[int],
+                                r: float = 0.15,
+                                strategies: Sequence[str] = ("lowfreq", "highfreq", "random",
+                                                             "none"),
+                                alpha: float = 0.5, seed: int = 0) -> dict:
+    """The recovery check of run_selection_experiment on a BASELINE geometry
+    (SURVEY.md §8(f) row 4): one request, chunks encoded in isolation, every
+    strategy at the same budget, suffix-row attention recorded on the device
+    (record_attention=<history>: the selective pass stays on the tensor-core
+    kernel, only the suffix rows' probabilities are materialised).  Returns
+    {strategy: deviation}."""
+    for s in strategies:
+        if s not in STRATEGIES:
+            raise InvalidPlan(f"unknown strategy {s!r}")
+    toks = [np.asarray(t, dtype=np.int64) for t in chunk_tokens]
+    suffix = np.asarray(suffix, dtype=np.int64)
+    history = int(sum(t.size for t in toks))
+    full = full_prefill(model, np.concatenate(toks + [suffix]), record_attention=history,
+                        logits_rows=None)
+    chunks = [encode_chunk_isolated(model, t, chunk_id=f"x{j}") for j, t in enumerate(toks)]
+    sel_rng = np.random.default_rng([seed, 2])
+    out = {}
+    for s in strategies:
+        rankings = [strategy_ranking(c, s, alpha, rng=sel_rng) for c in chunks]
+        sel = selective_prefill(model, chunks, rankings, suffix, effective_ratio(s, r),
+                                record_attention=history, logits_rows=None)
+        out[s] = attention_deviation(full.attention.suffix_view(history),
+                                     sel.attention.suffix_view(history))
+        del sel
+    return out
+
+
+def spectrum_report(chunk, n_bands: int = 10) -> dict:
+    """Energy fraction per frequency band for the chunk's Keys and Values
+    (ct/toymodel.py:315-341): conjugate-symmetric interior bins double-weighted,
+    bands [floor(b*F/n_bands), floor((b+1)*F/n_bands)).  A reporting helper,
+    off the hot path: the per-bin spectra come from cuFFT (torch.fft) in f64."""
+    if isinstance(chunk, DeviceChunk):
+        sides = (("key", chunk.keys), ("value", chunk.values))
+    else:
+        dev = _dev.require_cuda()
+        sides = (("key", torch.from_numpy(np.stack([np.asarray(t.data, np.float32)
+                                                    for t in chunk.keys_raw])).to(dev)),
+                 ("value", torch.from_numpy(np.stack([np.asarray(t.data, np.float32)
+                                                      for t in chunk.values])).to(dev)))
+    n = chunk.token_count
+    n_freqs = n // 2 + 1
+    weights = np.full(n_freqs, 2.0)
+    weights[0] = 1.0
+    if n % 2 == 0:
+        weights[-1] = 1.0
+    edges = [int(np.floor(b * n_freqs / n_bands)) for b in range(n_bands + 1)]
+    out = {}
+    for name, t in sides:
+        per_bin = np.zeros(n_freqs)
+        for l in range(t.shape[0]):  # layer by layer, in the reference's order
+            spec = torch.fft.rfft(t[l].double(), dim=0)
+            per_bin += (spec.abs() ** 2).reshape(n_freqs, -1).sum(dim=1).cpu().numpy()
+        per_bin *= weights
+        total = per_bin.sum()
+        bands = np.array([per_bin[edges[b]:edges[b + 1]].sum() for b in range(n_bands)])
+        out[name] = bands / total if total > 0 else bands
+    return out

@@ -60,19 +60,32 @@ class AttentionRecord:
 
     def suffix_view(self, suffix_start: int) -> "AttentionRecord":
         rows = np.flatnonzero(self.query_positions >= suffix_start)
-        mats = tuple(np.asarray(m)[:, rows, :suffix_start].copy() for m in self.matrices)
-        return AttentionRecord(mats, self.query_positions[rows].copy(), suffix_start)
+        mats = []
+        for m in self.matrices:
+            if isinstance(m, torch.Tensor):  # device record (record_attention=<position>)
+                idx = torch.as_tensor(rows, device=m.device)
+                mats.append(m.index_select(1, idx)[:, :, :suffix_start].contiguous())
+            else:
+                mats.append(np.asarray(m)[:, rows, :suffix_start].copy())
+        return AttentionRecord(tuple(mats), self.query_positions[rows].copy(), suffix_start)
 
 
 def attention_deviation(a: AttentionRecord, b: AttentionRecord) -> float:
-    """Mean Frobenius distance of two records (ct/toymodel.py:113-124)."""
+    """Mean Frobenius distance of two records (ct/toymodel.py:113-124); device
+    records are reduced on the device (f64 accumulation)."""
     if len(a.matrices) != len(b.matrices):
         raise ShapeError("records have different layer counts")
     total, count = 0.0, 0
     for ma, mb in zip(a.matrices, b.matrices):
-        ma, mb = np.asarray(ma), np.asarray(mb)
         if ma.shape != mb.shape:
-            raise ShapeError(f"attention shape mismatch {ma.shape} vs {mb.shape}")
+            raise ShapeError(f"attention shape mismatch {tuple(ma.shape)} vs {tuple(mb.shape)}")
+        if isinstance(ma, torch.Tensor) or isinstance(mb, torch.Tensor):
+            ta = torch.as_tensor(ma).double()
+            tb = torch.as_tensor(mb).to(ta.device).double()
+            total += float(torch.linalg.vector_norm(ta - tb, dim=(1, 2)).sum())
+            count += ma.shape[0]
+            continue
+        ma, mb = np.asarray(ma), np.asarray(mb)
         for h in range(ma.shape[0]):
             total += np.linalg.norm(ma[h] - mb[h])
             count += 1
@@ -98,6 +111,17 @@ def _auto_record(model: GpuModel, a: int, n_ctx: int, record) -> bool:
     if record is not None:
         return bool(record)
     return model.config.n_heads * a * n_ctx <= (1 << 26)
+
+
+def _record_mode(record):
+    """record_attention: None (auto) / bool (every query row, host record) / an
+    int position p (device record of the query rows at positions >= p only --
+    the suffix rows the quality check reads, ct/toymodel.py:104-110; the main
+    attention stays on the tensor-core kernel and the recorded rows are
+    recomputed with probabilities by the SIMT kernel)."""
+    if isinstance(record, (bool, type(None))):
+        return record, None
+    return False, int(record)
 
 
 class LayerBuffers:
@@ -129,12 +153,14 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
                caches: Sequence, reuse: Callable[[int], None] | None = None,
                record_attention: bool = False, logits_rows: str | None = "all",
                k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None,
-               timer=None, hook: Callable[[int, str], None] | None = None):
+               timer=None, hook: Callable[[int, str], None] | None = None,
+               record_rows_from: int | None = None):
     """Shared forward engine (ct/toymodel.py:135-193) over device inputs.
 
     tokens/positions: int32 [A] device.  caches[l] = (K, V) [n_ctx, Hkv, D]
     (model dtype).  reuse(l) fills the reused rows of layer l before its
-    attention.  Returns (logits f32 [rows, V] or None, probs list)."""
+    attention.  record_rows_from=i records probabilities of query rows [i, A)
+    only.  Returns (logits f32 [rows, V] or None, probs list)."""
     cfg = model.config
     dev = model.device
     a = tokens.numel()
@@ -179,6 +205,17 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
             timer.stop("attention", t0)
         if record_attention:
             probs_all.append(probs)
+        elif record_rows_from is not None and record_rows_from < a:
+            nr = a - record_rows_from
+            part = torch.empty((hq, nr, n_ctx), dtype=torch.float32, device=dev)
+            scratch = torch.empty((nr, hq * d), dtype=dt, device=dev)
+            wsr = lib.ct_attention_workspace_bytes(nr, hq, n_ctx, hkv, d, dtc)
+            _lib.check(lib.ct_selective_attention(
+                _dev.ptr(buf.q[record_rows_from:]), _dev.ptr(positions[record_rows_from:]), nr,
+                hq, _dev.ptr(kc), _dev.ptr(vc), n_ctx, hkv, d, kc.stride(0), scale, dtc,
+                _dev.ptr(scratch), dtc, _dev.ptr(part), _dev.ptr(_dev.workspace(wsr, "record")),
+                wsr, st), "ct_selective_attention")
+            probs_all.append(part)
         o = _mm_f32(buf.ctx, w["wo"])
         _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), _dev.ptr(o), _lib.CT_F32, a, hid,
                   NORM_EPS, _dev.ptr(buf.x), dtc, st)
@@ -228,7 +265,14 @@ def full_prefill(model, tokens: Sequence[int], *, record_attention=None,
     tok_d = torch.as_tensor(toks.astype(np.int32), device=dev)
     pos_d = torch.arange(n, dtype=torch.int32, device=dev)
     caches = _new_caches(g, n, dev)
-    rec = _auto_record(g, n, n, record_attention)
+    rec, rows_from = _record_mode(record_attention)
+    if rows_from is not None:
+        rows_from = min(max(rows_from, 0), n)
+        logits, probs = run_layers(g, tok_d, pos_d, n, caches, logits_rows=logits_rows,
+                                   record_rows_from=rows_from)
+        att = AttentionRecord(tuple(probs), np.arange(rows_from, n), n)
+        return PrefillResult(tuple(caches), att, logits, np.arange(n))
+    rec = _auto_record(g, n, n, rec)
     logits, probs = run_layers(g, tok_d, pos_d, n, caches, record_attention=rec,
                                logits_rows=logits_rows)
     att = (AttentionRecord(tuple(p.cpu().numpy() for p in probs), np.arange(n), n)
@@ -349,7 +393,14 @@ def selective_prefill(model, chunks: Sequence, rankings: Sequence, suffix_tokens
         return PrefillResult(tuple(caches), att,
                              torch.zeros((0, cfg.vocab_size), dtype=torch.float32, device=dev),
                              np.empty(0, np.int64))
-    rec_attn = _auto_record(g, a, n_ctx, record_attention)
+    rec_attn, rec_pos = _record_mode(record_attention)
+    if rec_pos is not None:
+        rows_from = int(np.searchsorted(qpos_host, rec_pos, side="left"))
+        logits, probs = run_layers(g, tokens, positions, n_ctx, caches, reuse=reuse,
+                                   logits_rows=logits_rows, record_rows_from=rows_from)
+        att = AttentionRecord(tuple(probs), qpos_host[rows_from:].copy(), n_ctx)
+        return PrefillResult(tuple(caches), att, logits, qpos_host)
+    rec_attn = _auto_record(g, a, n_ctx, rec_attn)
     logits, probs = run_layers(g, tokens, positions, n_ctx, caches, reuse=reuse,
                                record_attention=rec_attn, logits_rows=logits_rows)
     att = (AttentionRecord(tuple(p.cpu().numpy() for p in probs), qpos_host, n_ctx)

@@ -318,6 +318,23 @@ def experiment_cases(ct):
     np.savez_compressed(OUT / "experiment_cases.npz", **out)
 
 
+def spectrum_cases(ct):
+    """spectrum_report (ct/toymodel.py:315-341) on seeded chunks, incl. odd N."""
+    from cachetune import toymodel
+    rng = np.random.default_rng(4242)
+    out = {}
+    for i, (n, h, d, l, nb) in enumerate([(64, 2, 8, 2, 10), (33, 1, 4, 3, 4),
+                                          (256, 2, 16, 1, 10), (2, 1, 2, 1, 1)]):
+        keys = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(l)]
+        vals = [(rng.standard_normal((n, h, d)) + 3.0).astype(np.float32) for _ in range(l)]
+        rep = toymodel.spectrum_report(_chunk(ct, keys, vals), nb)
+        out[f"s{i}_keys"], out[f"s{i}_vals"] = np.stack(keys), np.stack(vals)
+        out[f"s{i}_bands"] = np.int64(nb)
+        out[f"s{i}_key"], out[f"s{i}_value"] = rep["key"], rep["value"]
+    out["count"] = np.int64(4)
+    np.savez_compressed(OUT / "spectrum_cases.npz", **out)
+
+
 def main():
     ct = _ref()
     if len(sys.argv) > 1:  # regenerate only the named fixtures
@@ -326,6 +343,7 @@ def main():
         return
     highband_cases(ct)
     experiment_cases(ct)
+    spectrum_cases(ct)
     ctkv_cases(ct)
     spectral_cases(ct)
     big_chunks(ct)
