@@ -179,57 +179,63 @@ __device__ __forceinline__ uint4 rot8_bf16(uint4 u, const float4 c01, const floa
   return u;
 }
 
-// Hot-path blend for bf16 caches with adjacent pairing: one 16-B chunk (8
-// elements = 4 rotation pairs of one head) per unit, UNR units per thread with
-// every load issued before any math so ~UNR x 64 B are in flight per thread.
-template <int UNR>
+// Hot-path blend for bf16 caches with adjacent pairing.  One thread owns one
+// 16-B column chunk c (4 rotation pairs) of one reused row and walks the row's
+// heads: the (cos, sin) of (pos, pairs 4c..4c+3) is loaded ONCE and shared by
+// all H heads (the table is per position, not per head), and all 2*HB K/V
+// loads of a head block are issued before any math, so 2*HB*16 B are in
+// flight per thread.  A warp covers 2 rows x 16 chunks: every load/store
+// instruction moves two contiguous 256-B row segments.
+template <int HB>
 __global__ void __launch_bounds__(256)
-blend_bf16_kernel(SegArray segs, int64_t src_row_stride, int upr, int cph,
+blend_bf16_kernel(SegArray segs, int64_t src_row_stride, int H, int cph,
                   const float4* __restrict__ table, int half, __nv_bfloat16* __restrict__ kc,
                   __nv_bfloat16* __restrict__ vc, int64_t cache_row_stride) {
   const ct_segment sg = segs.s[blockIdx.y];
-  const int64_t total = sg.rows * upr;
+  const int64_t total = sg.rows * cph;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
   const __nv_bfloat16* ks = reinterpret_cast<const __nv_bfloat16*>(sg.k);
   const __nv_bfloat16* vs = reinterpret_cast<const __nv_bfloat16*>(sg.v);
-  for (int64_t u0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u0 < total;
-       u0 += nthr * UNR) {
-    uint4 kr[UNR], vr[UNR];
-    float4 c0[UNR], c1[UNR];
-    int64_t dst[UNR];
+  const int D = 8 * cph;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += nthr) {
+    const int64_t row = u / cph;
+    const int c = (int)(u - row * cph);
+    const int32_t tk = __ldg(sg.tok + row);
+    const int64_t pos = sg.pos0 + tk;
+    const int64_t srow = sg.src_by_tok ? (int64_t)tk : row;
+    const float4* t = table + (pos * half + 4 * c) / 2;
+    const float4 c0 = __ldg(t), c1 = __ldg(t + 1);
+    const uint4* kin = reinterpret_cast<const uint4*>(ks + srow * src_row_stride + 8 * c);
+    const uint4* vin = reinterpret_cast<const uint4*>(vs + srow * src_row_stride + 8 * c);
+    uint4* kout = reinterpret_cast<uint4*>(kc + pos * cache_row_stride + 8 * c);
+    uint4* vout = reinterpret_cast<uint4*>(vc + pos * cache_row_stride + 8 * c);
+    const int hstride = D / 8;  // uint4 per head
+    for (int h0 = 0; h0 < H; h0 += HB) {
+      uint4 kr[HB], vr[HB];
 #pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      const int64_t u = u0 + k * nthr;
-      dst[k] = -1;
-      if (u < total) {
-        const int64_t row = u / upr;
-        const int w = (int)(u - row * upr);
-        const int32_t tk = __ldg(sg.tok + row);
-        const int64_t pos = sg.pos0 + tk;
-        const int64_t srow = sg.src_by_tok ? (int64_t)tk : row;
-        kr[k] = __ldg(reinterpret_cast<const uint4*>(ks + srow * src_row_stride) + w);
-        vr[k] = __ldg(reinterpret_cast<const uint4*>(vs + srow * src_row_stride) + w);
-        const int j0 = (w % cph) * 4;  // first pair of this chunk within the head
-        const float4* t = table + (pos * half + j0) / 2;
-        c0[k] = __ldg(t);
-        c1[k] = __ldg(t + 1);
-        dst[k] = pos * cache_row_stride + (int64_t)w * 8;
+      for (int h = 0; h < HB; ++h) {
+        if (h0 + h < H) {
+          kr[h] = ldg_stream(kin + (h0 + h) * hstride);
+          vr[h] = ldg_stream(vin + (h0 + h) * hstride);
+        }
       }
-    }
 #pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      if (dst[k] >= 0) {
-        *reinterpret_cast<uint4*>(kc + dst[k]) = rot8_bf16(kr[k], c0[k], c1[k]);
-        *reinterpret_cast<uint4*>(vc + dst[k]) = vr[k];
+      for (int h = 0; h < HB; ++h) {
+        if (h0 + h < H) {
+          kout[(h0 + h) * hstride] = rot8_bf16(kr[h], c0, c1);
+          vout[(h0 + h) * hstride] = vr[h];
+        }
       }
     }
   }
 }
 
-// Hot-path QKV epilogue for bf16 in/out, adjacent pairing: 16-B chunks of the
-// qkv row; q chunks -> q_out (rotated), k -> cache (rotated) + optional raw
-// copy, v -> cache.
-template <int UNR>
+// Hot-path QKV epilogue for bf16 in/out, adjacent pairing.  One thread owns
+// 16-B column chunk c of a block of HB consecutive heads of one qkv row; the
+// (cos, sin) of (pos, pairs 4c..4c+3) is loaded once per thread and shared by
+// the block's q/k heads.  q heads -> q_out (rotated), k -> cache (rotated) +
+// optional raw copy, v -> cache.
+template <int HB>
 __global__ void __launch_bounds__(256)
 qkv_bf16_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld_qkv,
                 const int32_t* __restrict__ positions, int64_t A, int Hq, int Hkv, int D,
@@ -237,52 +243,43 @@ qkv_bf16_kernel(const __nv_bfloat16* __restrict__ qkv, int64_t ld_qkv,
                 __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
                 int64_t crs, __nv_bfloat16* __restrict__ k_raw) {
   const int cph = D / 8;
-  const int upr = (Hq + 2 * Hkv) * cph;
+  const int hpr = Hq + 2 * Hkv;
+  const int ng = (hpr + HB - 1) / HB;
   const int half = D / 2;
-  const int64_t total = A * upr;
+  const int64_t total = A * ng * cph;
   const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t u0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u0 < total;
-       u0 += nthr * UNR) {
-    uint4 x[UNR];
-    float4 c0[UNR], c1[UNR];
-    int64_t a_[UNR], pos_[UNR];
-    int w_[UNR];
-#pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      const int64_t u = u0 + k * nthr;
-      a_[k] = -1;
-      if (u < total) {
-        const int64_t a = u / upr;
-        const int w = (int)(u - a * upr);
-        const int64_t pos = __ldg(positions + a);
-        x[k] = __ldg(reinterpret_cast<const uint4*>(qkv + a * ld_qkv) + w);
-        if (w < (Hq + Hkv) * cph) {
-          const int j0 = (w % cph) * 4;
-          const float4* t = table + (pos * half + j0) / 2;
-          c0[k] = __ldg(t);
-          c1[k] = __ldg(t + 1);
-        }
-        a_[k] = a;
-        pos_[k] = pos;
-        w_[k] = w;
-      }
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total; u += nthr) {
+    const int64_t ag = u / cph;
+    const int c = (int)(u - ag * cph);
+    const int64_t a = ag / ng;
+    const int h0 = (int)(ag - a * ng) * HB;
+    const int64_t pos = __ldg(positions + a);
+    const uint4* in = reinterpret_cast<const uint4*>(qkv + a * ld_qkv + 8 * c);
+    float4 c0 = make_float4(0.f, 0.f, 0.f, 0.f), c1 = c0;
+    if (h0 < Hq + Hkv) {
+      const float4* t = table + (pos * half + 4 * c) / 2;
+      c0 = __ldg(t);
+      c1 = __ldg(t + 1);
     }
+    uint4 x[HB];
 #pragma unroll
-    for (int k = 0; k < UNR; ++k) {
-      if (a_[k] < 0) continue;
-      const int w = w_[k];
-      const int hh = w / cph, c = w % cph;
+    for (int h = 0; h < HB; ++h)
+      if (h0 + h < hpr) x[h] = ldg_stream(in + (h0 + h) * cph);
+#pragma unroll
+    for (int h = 0; h < HB; ++h) {
+      const int hh = h0 + h;
+      if (hh >= hpr) break;
       if (hh >= Hq + Hkv) {
-        *reinterpret_cast<uint4*>(vc + pos_[k] * crs + (int64_t)(hh - Hq - Hkv) * D + c * 8) = x[k];
+        *reinterpret_cast<uint4*>(vc + pos * crs + (int64_t)(hh - Hq - Hkv) * D + c * 8) = x[h];
         continue;
       }
-      const uint4 r = rot8_bf16(x[k], c0[k], c1[k]);
+      const uint4 r = rot8_bf16(x[h], c0, c1);
       if (hh < Hq) {
-        *reinterpret_cast<uint4*>(q_out + (a_[k] * Hq + hh) * (int64_t)D + c * 8) = r;
+        *reinterpret_cast<uint4*>(q_out + (a * Hq + hh) * (int64_t)D + c * 8) = r;
       } else {
-        *reinterpret_cast<uint4*>(kc + pos_[k] * crs + (int64_t)(hh - Hq) * D + c * 8) = r;
+        *reinterpret_cast<uint4*>(kc + pos * crs + (int64_t)(hh - Hq) * D + c * 8) = r;
         if (k_raw)
-          *reinterpret_cast<uint4*>(k_raw + (a_[k] * Hkv + hh - Hq) * (int64_t)D + c * 8) = x[k];
+          *reinterpret_cast<uint4*>(k_raw + (a * Hkv + hh - Hq) * (int64_t)D + c * 8) = x[h];
       }
     }
   }
@@ -468,16 +465,15 @@ extern "C" int ct_gather_rope_blend(const ct_segment* segs, int n_segs, int64_t 
   for (int i = 0; i < n_segs && fast; ++i)
     fast = ((uintptr_t)segs[i].k % 16 == 0) && ((uintptr_t)segs[i].v % 16 == 0);
   if (fast) {
-    constexpr int UNR = 4;
-    const int upr = (int)(H * D / 8);
-    int64_t bx = (max_rows * upr + 256 * UNR - 1) / (256 * UNR);
-    const int64_t cap = (148 * 8 + n_segs - 1) / n_segs;
+    const int cph = (int)(D / 8);
+    int64_t bx = (max_rows * cph + 255) / 256;
+    const int64_t cap = (148 * 16 + n_segs - 1) / n_segs;
     if (bx > cap) bx = cap;
     dim3 grid((unsigned)bx, (unsigned)n_segs);
-    blend_bf16_kernel<UNR><<<grid, 256, 0, st>>>(arr, src_row_stride, upr, (int)(D / 8),
-                                                 (const float4*)table, (int)(D / 2),
-                                                 (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache,
-                                                 cache_row_stride);
+    blend_bf16_kernel<8><<<grid, 256, 0, st>>>(arr, src_row_stride, (int)H, cph,
+                                               (const float4*)table, (int)(D / 2),
+                                               (__nv_bfloat16*)k_cache, (__nv_bfloat16*)v_cache,
+                                               cache_row_stride);
     return check_launch("blend_bf16_kernel");
   }
   const bool v4 = (D / 2) % 4 == 0;
@@ -522,11 +518,10 @@ extern "C" int ct_qkv_rope_scatter(const void* qkv, int64_t ld_qkv, int in_dtype
       cache_row_stride % 8 == 0 &&
       (((uintptr_t)qkv | (uintptr_t)q_out | (uintptr_t)k_cache | (uintptr_t)v_cache |
         (uintptr_t)table | (uintptr_t)k_raw_out) % 16 == 0)) {
-    constexpr int UNR = 4;
-    const int64_t units = A * (Hq + 2 * Hkv) * (D / 8);
-    int64_t g = (units + 256 * UNR - 1) / (256 * UNR);
+    const int64_t units = A * ((Hq + 2 * Hkv + 7) / 8) * (D / 8);
+    int64_t g = (units + 255) / 256;
     if (g > 148 * 16) g = 148 * 16;
-    qkv_bf16_kernel<UNR><<<(unsigned)g, 256, 0, st>>>(
+    qkv_bf16_kernel<8><<<(unsigned)g, 256, 0, st>>>(
         (const __nv_bfloat16*)qkv, ld_qkv, positions, A, (int)Hq, (int)Hkv, (int)D,
         (const float4*)table, (__nv_bfloat16*)q_out, (__nv_bfloat16*)k_cache,
         (__nv_bfloat16*)v_cache, cache_row_stride, (__nv_bfloat16*)k_raw_out);

@@ -48,6 +48,15 @@ template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(flo
   return __float2bfloat16_rn(x);
 }
 
+// 16-B read-once load: bypasses L1 (the source row is not re-read by this CTA).
+__device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
 inline bool valid_dtype(int d) { return d == CT_F32 || d == CT_BF16; }
 inline size_t dtype_size(int d) { return d == CT_BF16 ? 2 : (d == CT_F64 ? 8 : 4); }
 

@@ -270,6 +270,280 @@ fft_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values,
   }
 }
 
+// ---------------------------------------------------------------------------
+// v2 energy kernel for N = 256*R3 (512..4096): register-resident Stockham FFT.
+//
+// A group of GT = N/16 threads owns one packed signal (2 lanes); every thread
+// holds 16 complex points in registers.  Forward radices (16, 16, R3), inverse
+// (R3, 16, 16): the forward's last pass leaves thread t holding exactly the
+// bins j + (N/R3) r its inverse first pass needs, so the low-pass mask and the
+// spectrum never touch shared memory.  Four exchanges per signal (f1->f2,
+// f2->f3, i1->i2, i2->i3) go through a padded per-group buffer; the inverse's
+// last pass leaves token t + GT r in register r, so |recon|^2 accumulates in
+// registers over all of the CTA's signals.  Input lanes arrive as a [N][2*NG]
+// tile staged with cp.async one tile ahead.  Twiddles: W^a, W^2a, W^4a, W^8a
+// from the table, the other powers as products (depth <= 3).
+// ---------------------------------------------------------------------------
+constexpr int FFT2_THREADS = 512;
+
+template <typename T> struct tconst;
+template <> struct tconst<double> {
+  static constexpr double h = 0.70710678118654752440, c1 = 0.92387953251128675613,
+                          s1 = 0.38268343236508977173;
+};
+template <> struct tconst<float> {
+  static constexpr float h = 0.70710678118654752440f, c1 = 0.92387953251128675613f,
+                         s1 = 0.38268343236508977173f;
+};
+
+// 16-point DFT in place, natural order in and out (4 x 4 with W16 twiddles).
+template <bool INV, typename T>
+__device__ __forceinline__ void dft16(cpx<T>* v) {
+  cpx<T> a[4][4];
+#pragma unroll
+  for (int n1 = 0; n1 < 4; ++n1) {
+    cpx<T> t[4] = {v[n1], v[n1 + 4], v[n1 + 8], v[n1 + 12]};
+    dft_small<4, INV>(t);
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) a[n1][k2] = t[k2];
+  }
+  const T h = tconst<T>::h, c1 = tconst<T>::c1, s1 = tconst<T>::s1;
+  const T sg = INV ? (T)1 : (T)-1;  // sign of the imaginary part of W16^1
+  // W16^e for e = n1*k2
+  a[1][1] = cmul(a[1][1], cpx<T>{c1, sg * s1});
+  a[1][2] = cmul(a[1][2], cpx<T>{h, sg * h});
+  a[1][3] = cmul(a[1][3], cpx<T>{s1, sg * c1});
+  a[2][1] = cmul(a[2][1], cpx<T>{h, sg * h});
+  a[2][2] = mul_mi<INV>(a[2][2]);
+  a[2][3] = cmul(a[2][3], cpx<T>{-h, sg * h});
+  a[3][1] = cmul(a[3][1], cpx<T>{s1, sg * c1});
+  a[3][2] = cmul(a[3][2], cpx<T>{-h, sg * h});
+  a[3][3] = cmul(a[3][3], cpx<T>{-c1, -sg * s1});
+#pragma unroll
+  for (int k2 = 0; k2 < 4; ++k2) {
+    cpx<T> t[4] = {a[0][k2], a[1][k2], a[2][k2], a[3][k2]};
+    dft_small<4, INV>(t);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) v[k2 + 4 * k1] = t[k1];
+  }
+}
+
+template <int R, bool INV, typename T>
+__device__ __forceinline__ void dft_r(cpx<T>* v) {
+  if constexpr (R == 16) dft16<INV>(v);
+  else dft_small<R, INV>(v);
+}
+
+template <bool INV, typename T>
+__device__ __forceinline__ cpx<T> twl(const cpx<T>* __restrict__ tw, int idx) {
+  cpx<T> w = tw[idx];
+  if (INV) w.y = -w.y;
+  return w;
+}
+
+// v[r] *= W_N^{(a*r) mod N} (conjugated for INV), r = 1..R-1.
+template <int R, bool INV, int N, typename T>
+__device__ __forceinline__ void twiddle(cpx<T>* v, const cpx<T>* __restrict__ tw, int a) {
+  if (a == 0) return;
+  cpx<T> w[16];
+  w[1] = twl<INV>(tw, a & (N - 1));
+  if constexpr (R > 2) {
+    w[2] = twl<INV>(tw, (2 * a) & (N - 1));
+    w[3] = cmul(w[1], w[2]);
+  }
+  if constexpr (R > 4) {
+    w[4] = twl<INV>(tw, (4 * a) & (N - 1));
+    w[5] = cmul(w[1], w[4]);
+    w[6] = cmul(w[2], w[4]);
+    w[7] = cmul(w[3], w[4]);
+  }
+  if constexpr (R > 8) {
+    w[8] = twl<INV>(tw, (8 * a) & (N - 1));
+#pragma unroll
+    for (int r = 9; r < 16; ++r) w[r] = cmul(w[r - 8], w[8]);
+  }
+#pragma unroll
+  for (int r = 1; r < R; ++r) v[r] = cmul(v[r], w[r]);
+}
+
+// Exchange-buffer index.  16-B elements (f64 complex) are served 8 threads per
+// shared-memory wavefront: an XOR of the low 3 index bits with bits 3-6 keeps
+// every exchange pattern (stride 1, 16, R3 and the Stockham output scatter)
+// conflict-free without padding.  8-B elements (f32 complex, 16 threads per
+// wavefront) use one pad element per 16.
+template <typename T>
+__device__ __forceinline__ int sp16(int i) {
+  if constexpr (sizeof(T) == 8) return i ^ (((i >> 3) ^ (i >> 4)) & 7);
+  else return i + (i >> 4);
+}
+
+template <int GT>
+__device__ __forceinline__ void group_sync(int g) {
+  if constexpr (GT == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(GT) : "memory");
+  }
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+template <typename T, typename IN, int R3>
+struct Fft2Cfg {
+  static constexpr int N = 256 * R3;
+  static constexpr int GT = N / 16;                 // threads per signal group
+  static constexpr int NG = FFT2_THREADS / GT;      // signals per tile
+  static constexpr int TW = 2 * NG;                 // lanes per tile
+  static constexpr int SIGPAD = sizeof(T) == 8 ? N : N + N / 16;  // group buffer (elements)
+  static constexpr size_t SIG_BYTES = (size_t)NG * SIGPAD * sizeof(cpx<T>);
+  static constexpr size_t TILE_BYTES = (size_t)N * TW * sizeof(IN);
+  static constexpr size_t ACC_BYTES = (size_t)N * sizeof(double);
+  static constexpr size_t SMEM = SIG_BYTES + TILE_BYTES + ACC_BYTES;
+  static_assert(NG * N == 8192, "8192 points in flight per CTA");
+};
+
+// Stage tile `it` (lanes lt0 .. lt0+TW) of rows [0, N) into smem.
+template <typename IN, int N, int TW>
+__device__ __forceinline__ void load_tile(IN* tile, const IN* base, int64_t ld_token, int lt0,
+                                          int lane_end, bool vec_ok) {
+  constexpr int CPR = TW * (int)sizeof(IN) / 16;  // 16-B chunks per row
+  constexpr bool whole = (TW * sizeof(IN)) % 16 == 0;
+  if (whole && vec_ok && lt0 + TW <= lane_end) {
+    for (int q = threadIdx.x; q < N * CPR; q += FFT2_THREADS) {
+      const int n = q / CPR, ch = q % CPR;
+      cp_async16(reinterpret_cast<char*>(tile) + (size_t)q * 16,
+                 reinterpret_cast<const char*>(base + (int64_t)n * ld_token + lt0) + ch * 16);
+    }
+  } else {
+    for (int q = threadIdx.x; q < N * TW; q += FFT2_THREADS) {
+      const int n = q / TW, c = q % TW;
+      const int lane = lt0 + c;
+      tile[q] = lane < lane_end ? base[(int64_t)n * ld_token + lane] : IN(0.0f);
+    }
+  }
+  cp_async_commit();
+}
+
+template <typename T, typename IN, int R3>
+__global__ void __launch_bounds__(FFT2_THREADS, 1)
+fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int L, int lanes,
+                   int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff,
+                   const cpx<T>* __restrict__ tw, double* __restrict__ partial) {
+  using Cfg = Fft2Cfg<T, IN, R3>;
+  constexpr int N = Cfg::N, GT = Cfg::GT, NG = Cfg::NG, TW = Cfg::TW;
+  constexpr int Q = 16 / R3;          // radix-R3 butterflies per thread
+  constexpr int NR3 = N / R3;         // = 256
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cpx<T>* sigall = reinterpret_cast<cpx<T>*>(smem_raw);
+  IN* tile = reinterpret_cast<IN*>(smem_raw + Cfg::SIG_BYTES);
+  // per-token energy of the CTA's signals, summed group by group in a fixed
+  // order (registers hold the FFT; a per-thread f64 accumulator would spill)
+  double* acc = reinterpret_cast<double*>(smem_raw + Cfg::SIG_BYTES + Cfg::TILE_BYTES);
+
+  const int g = threadIdx.x / GT, t = threadIdx.x % GT;
+  cpx<T>* sig = sigall + g * Cfg::SIGPAD;
+  const int lb = blockIdx.x, tensor = blockIdx.y;
+  const int c = blockIdx.z / L, l = blockIdx.z % L;
+  const IN* base = (tensor == 0 ? keys : values) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer;
+  const int lane0 = lb * LANE_BLOCK;
+  const int lane_end = min(lanes, lane0 + LANE_BLOCK);
+  const int iters = (lane_end - lane0 + TW - 1) / TW;
+  const bool vec_ok = ((ld_token * (int64_t)sizeof(IN)) % 16 == 0) &&
+                      (((uintptr_t)base) % 16 == 0) && ((lane0 * (int)sizeof(IN)) % 16 == 0);
+
+  for (int n = threadIdx.x; n < N; n += FFT2_THREADS) acc[n] = 0.0;
+  load_tile<IN, N, TW>(tile, base, ld_token, lane0, lane_end, vec_ok);
+  cp_async_wait_all();
+  __syncthreads();
+  for (int it = 0; it < iters; ++it) {
+    cpx<T> v[16];
+    // f1 input: lanes (2g, 2g+1) of tokens t + GT r
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const IN* p = tile + (size_t)(t + GT * r) * TW + 2 * g;
+      v[r] = {(T)to_f32(p[0]), (T)to_f32(p[1])};
+    }
+    __syncthreads();
+    if (it + 1 < iters)
+      load_tile<IN, N, TW>(tile, base, ld_token, lane0 + (it + 1) * TW, lane_end, vec_ok);
+
+    // ---- forward f1: radix 16, Ns = 1
+    dft16<false>(v);
+    group_sync<GT>(g);  // previous signal's i3 reads of sig are done
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sig[sp16<T>(16 * t + r)] = v[r];
+    group_sync<GT>(g);
+    // ---- f2: radix 16, Ns = 16
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = sig[sp16<T>(t + GT * r)];
+    twiddle<16, false, N>(v, tw, (t & 15) * R3);
+    dft16<false>(v);
+    group_sync<GT>(g);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sig[sp16<T>((t >> 4) * 256 + (t & 15) + 16 * r)] = v[r];
+    group_sync<GT>(g);
+    // ---- f3: radix R3, Ns = N/R3; mask; i1: inverse radix R3, Ns = 1
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = t + q * GT;
+      cpx<T>* w = v + q * R3;
+#pragma unroll
+      for (int r = 0; r < R3; ++r) w[r] = sig[sp16<T>(j + NR3 * r)];
+      twiddle<R3, false, N>(w, tw, j);
+      dft_r<R3, false>(w);
+#pragma unroll
+      for (int r = 0; r < R3; ++r) {
+        const int k = j + NR3 * r;
+        const int kk = k < N - k ? k : N - k;
+        if (cutoff >= 0 ? kk >= cutoff : kk < -cutoff - 1) w[r] = {(T)0, (T)0};
+      }
+      dft_r<R3, true>(w);
+    }
+    group_sync<GT>(g);
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const int j = t + q * GT;
+#pragma unroll
+      for (int r = 0; r < R3; ++r) sig[sp16<T>(j * R3 + r)] = v[q * R3 + r];
+    }
+    group_sync<GT>(g);
+    // ---- i2: inverse radix 16, Ns = R3
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = sig[sp16<T>(t + GT * r)];
+    twiddle<16, true, N>(v, tw, (t % R3) * 16);
+    dft16<true>(v);
+    group_sync<GT>(g);
+#pragma unroll
+    for (int r = 0; r < 16; ++r) sig[sp16<T>((t / R3) * (16 * R3) + (t % R3) + R3 * r)] = v[r];
+    group_sync<GT>(g);
+    // ---- i3: inverse radix 16, Ns = N/16 -> token t + GT r in v[r]
+#pragma unroll
+    for (int r = 0; r < 16; ++r) v[r] = sig[sp16<T>(t + GT * r)];
+    twiddle<16, true, N>(v, tw, t);
+    dft16<true>(v);
+    double e[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) e[r] = (double)(v[r].x * v[r].x + v[r].y * v[r].y);
+    cp_async_wait_all();  // next tile landed (its barrier is the last one below)
+    for (int q = 0; q < NG; ++q) {
+      if (g == q) {
+#pragma unroll
+        for (int r = 0; r < 16; ++r) acc[t + GT * r] += e[r];
+      }
+      __syncthreads();
+    }
+  }
+  const double inv_n2 = 1.0 / ((double)N * (double)N);
+  const int nlb = gridDim.x;
+  double* out = partial + ((((int64_t)blockIdx.z * 2 + tensor) * nlb) + lb) * N;
+  for (int n = threadIdx.x; n < N; n += FFT2_THREADS) out[n] = acc[n] * inv_n2;
+}
+
 // Circulant band kernel p[m] = (1/N) sum_{k in band} w_k cos(2 pi k m/N) over
 // rfft bins k in [0, N/2] (w_k = 1 for DC and an even-N Nyquist bin, else 2):
 // the exact impulse response of rfft -> zero the other bins -> irfft.  Low band
@@ -500,10 +774,35 @@ static int launch_fft_t(const void* k, const void* v, int L, int C, int lanes, i
   return check_launch("fft_energy_kernel");
 }
 
+template <typename T, typename IN, int R3>
+static int launch_fft2_t(const void* k, const void* v, int L, int C, int lanes, int64_t ldt,
+                         int64_t ldl, int64_t ldc, int cutoff, const void* tw, double* partial,
+                         cudaStream_t st) {
+  using Cfg = Fft2Cfg<T, IN, R3>;
+  auto kern = fft2_energy_kernel<T, IN, R3>;
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+  const int nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
+  dim3 grid(nlb, 2, C * L);
+  kern<<<grid, FFT2_THREADS, Cfg::SMEM, st>>>((const IN*)k, (const IN*)v, L, lanes, ldt, ldl, ldc,
+                                              cutoff, (const cpx<T>*)tw, partial);
+  return check_launch("fft2_energy_kernel");
+}
+
+static bool g_fft_v1_only = getenv("CT_SCORER_V1") != nullptr;
+
 template <typename T, typename IN>
 static int launch_fft(int logn, const void* k, const void* v, int L, int C, int lanes,
                       int64_t ldt, int64_t ldl, int64_t ldc, int cutoff, const void* tw,
                       double* partial, cudaStream_t st) {
+  if (!g_fft_v1_only) {
+    switch (logn) {
+      case 9: return launch_fft2_t<T, IN, 2>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+      case 10: return launch_fft2_t<T, IN, 4>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+      case 11: return launch_fft2_t<T, IN, 8>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+      case 12: return launch_fft2_t<T, IN, 16>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+      default: break;
+    }
+  }
   switch (logn) {
 #define CT_CASE(LG) \
   case LG: return launch_fft_t<T, IN, LG>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);

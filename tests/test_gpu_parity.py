@@ -119,6 +119,31 @@ def test_big_chunks_config2_geometry(ct, precision):
         assert np.array_equal(outb["agg_order"][0].cpu().numpy(), g[f"s{s}_bf16_agg"])
 
 
+@pytest.mark.parametrize("n", [512, 1024, 2048, 4096])
+@pytest.mark.parametrize("lanes", [(2, 8), (13, 10)])
+@pytest.mark.parametrize("alpha", [0.5, 0.13, 1.0])
+def test_scorer_fft_lengths_vs_oracle(ct, n, lanes, alpha):
+    """Register-resident Stockham path (N = 512..4096) incl. ragged lane counts
+    (lanes not a multiple of the tile width / 128-lane block) vs the oracle."""
+    from paper_2605_24022_b200.spectral import score_device
+    h, d = lanes
+    rng = np.random.default_rng(n + h + int(alpha * 100))
+    L = 2
+    keys = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(L)]
+    vals = [rng.standard_normal((n, h, d)).astype(np.float32) for _ in range(L)]
+    k = torch.from_numpy(np.stack(keys))[None].cuda()
+    v = torch.from_numpy(np.stack(vals))[None].cuda()
+    out = score_device(k, v, alpha, "f64")
+    for layer in range(L):
+        want = O.low_freq_scores(keys[layer], vals[layer], alpha)
+        got = out["layer_scores"][0, layer].cpu().numpy()
+        np.testing.assert_allclose(got, want, rtol=1e-11, atol=1e-13 * float(want.max()))
+        assert np.array_equal(out["layer_order"][0, layer].cpu().numpy(), O.descending_order(want))
+    out32 = score_device(k, v, alpha, "f32")
+    np.testing.assert_allclose(out32["layer_scores"].cpu().numpy(),
+                               out["layer_scores"].cpu().numpy(), rtol=2e-5)
+
+
 def test_batched_chunks_and_selection_plan(ct):
     from paper_2605_24022_b200.spectral import score_device, select_device
     rng = np.random.default_rng(7)
