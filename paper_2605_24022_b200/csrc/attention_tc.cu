@@ -34,14 +34,22 @@ constexpr int ATOM_BYTES = 128 * 64 * 2;      // [128 rows][64 bf16] swizzle-128
 constexpr int TILE_BYTES = 2 * ATOM_BYTES;    // 32 KiB: 128 rows x 128 bf16
 constexpr float LAZY_THRESH = 8.0f;           // log2 units
 
+// CTAS = 1: one CTA owns a 128-row tile and stages whole K/V tiles (32 KiB).
+// CTAS = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2, MMA M = 256)
+// owns two 128-row tiles; each CTA stages HALF of every K tile (64 keys) and
+// half of every V tile (64 head-dim columns), 16 KiB per slot, so per SM the
+// K/V bytes from L2 and the MMA operand reads from shared memory halve.
+template <int CTAS>
 struct Smem {
+  static constexpr int SLOT_BYTES = TILE_BYTES / CTAS;
+  static constexpr int SLOTS = CTAS == 1 ? KV_SLOTS : 2 * KV_SLOTS;
   // offsets from the 1024-aligned base
   static constexpr int Q = 0;
   static constexpr int KV = Q + TILE_BYTES;
-  static constexpr int BAR = KV + KV_SLOTS * TILE_BYTES;
+  static constexpr int BAR = KV + SLOTS * SLOT_BYTES;
   // q + KV full/empty + per S/P buffer (S full, P full, PV done); the
   // exchange area must not overlap the last barrier
-  static constexpr int NBAR = 1 + 2 * KV_SLOTS + 3 * 3;
+  static constexpr int NBAR = 1 + 2 * SLOTS + 3 * 3;
   static constexpr int XCH = BAR + NBAR * 8;  // [3][MAX_SPLIT][128] f32 max/sum exchange
   static constexpr int TMEM_PTR = XCH + 3 * MAX_SPLIT * 128 * 4;
   static constexpr int TOTAL = TMEM_PTR + 16;
@@ -79,6 +87,95 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
 }
+// 2-SM TMA: bytes land in this CTA's smem, completion counts on the LEADER's
+// mbarrier (same offset, peer bit cleared).
+__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                                int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(map), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// shared::cluster address of the same smem offset in CTA `rank`
+__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAITC:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONEC;\n\t"
+      "bra LAB_WAITC;\n\t"
+      "DONEC:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+template <int CTAS>
+__device__ __forceinline__ void tc_commit_t(uint32_t bar) {
+  if constexpr (CTAS == 1) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], m;\n\t}" ::"r"(bar)
+        : "memory");
+  }
+}
+template <int CTAS>
+__device__ __forceinline__ void tc_mma_t(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accum) {
+  if constexpr (CTAS == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  }
+}
+template <int CTAS>
+__device__ __forceinline__ void tc_mma_ts_t(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accum) {
+  if constexpr (CTAS == 1) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  } else {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
+        : "memory");
+  }
+}
+
 __device__ __forceinline__ void tc_fence_before() {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -172,10 +269,10 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo_bytes, uin
   return d;
 }
 
-// Instruction descriptor: kind::f16, bf16 A/B, f32 D, M=128, N=128.
-__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major) {
+// Instruction descriptor: kind::f16, bf16 A/B, f32 D, M = 128*CTAS, N=128.
+__host__ __device__ constexpr uint32_t idesc_bf16(bool b_mn_major, int m = TILE_M) {
   return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
-         ((uint32_t)(BLK_N >> 3) << 17) | ((uint32_t)(TILE_M >> 4) << 24);
+         ((uint32_t)(BLK_N >> 3) << 17) | ((uint32_t)(m >> 4) << 24);
 }
 
 __device__ __forceinline__ float ex2(float x) {
@@ -281,7 +378,7 @@ struct Params {
   float lazy_thresh;
 };
 
-template <int NSPLIT, uint32_t POLY_MASK>
+template <int NSPLIT, uint32_t POLY_MASK, int EXPT = 0, int CTAS = 1>
 __global__ void __launch_bounds__(32 * (4 * NSPLIT + 2), 1)
 attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
@@ -290,61 +387,88 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
   constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
   constexpr int HALF = BLK_N / NSPLIT;  // key columns per softmax thread
   constexpr int NSM = 32 * SOFTMAX_WARPS;
+  using SM = Smem<CTAS>;
+  constexpr int NSLOT = SM::SLOTS;
+  constexpr int SLOT = SM::SLOT_BYTES;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sQ = base + Smem::Q, sKV = base + Smem::KV;
-  const uint32_t bar0 = base + Smem::BAR;
+  const uint32_t sQ = base + SM::Q, sKV = base + SM::KV;
+  const uint32_t bar0 = base + SM::BAR;
+  const uint32_t crank = CTAS == 2 ? cluster_rank() : 0u;
+  const bool leader = crank == 0;
   // barriers
   const uint32_t bar_q = bar0 + 0 * 8;
   auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };
-  auto bar_empty = [&](int s) { return bar0 + (1 + KV_SLOTS + s) * 8; };
-  constexpr int B2 = 1 + 2 * KV_SLOTS;
+  auto bar_empty = [&](int s) { return bar0 + (1 + NSLOT + s) * 8; };
+  constexpr int B2 = 1 + 2 * NSLOT;
   // per S/P TMEM buffer (3): S landed, P written, PV (the reader of P) done
   auto bar_sfull = [&](int b) { return bar0 + (B2 + b) * 8; };
   auto bar_pfull = [&](int b) { return bar0 + (B2 + 3 + b) * 8; };
   auto bar_pvdone = [&](int b) { return bar0 + (B2 + 6 + b) * 8; };
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + Smem::TMEM_PTR);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + SM::TMEM_PTR);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // longest tiles first: high query blocks (largest positions) get low block ids
-  const int tile = blockIdx.x;
-  const int qb = p.n_qblocks - 1 - (tile / p.Hkv);
+  // longest tiles first: high query blocks (largest positions) get low block
+  // ids.  A CTA pair takes two adjacent query blocks of one kv head.
+  const int tile = blockIdx.x / CTAS;
+  const int n_units = (p.n_qblocks + CTAS - 1) / CTAS;
+  const int qb0 = (n_units - 1 - (tile / p.Hkv)) * CTAS;
+  const int qb = qb0 + (int)crank;
   const int g = tile % p.Hkv;
   const int a0 = qb * p.QB;
 
+  // key range: the pair shares every K/V block, so both use the pair's max
   int maxpos = 0;
-  for (int i = 0; i < p.QB; ++i) {
-    const int a = a0 + i;
+  for (int i = 0; i < CTAS * p.QB; ++i) {
+    const int a = qb0 * p.QB + i;
     if (a < p.A) maxpos = max(maxpos, __ldg(p.qpos + a));
   }
   maxpos = min(maxpos, p.n_ctx - 1);
   const int nb = maxpos / BLK_N + 1;
 
   if (threadIdx.x == 0) {
-    mbar_init(bar_q, 1);
-    for (int s = 0; s < KV_SLOTS; ++s) {
-      mbar_init(bar_full(s), 1);
+    // full / q: the leader's copies count one arrive per CTA of the pair (the
+    // leader's carries expect_tx for both CTAs' bytes); pfull: one elected
+    // arrive per softmax warp of every CTA of the pair
+    mbar_init(bar_q, CTAS);
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(bar_full(s), CTAS);
       mbar_init(bar_empty(s), 1);
     }
     for (int b = 0; b < NSB; ++b) {
       mbar_init(bar_sfull(b), 1);
-      mbar_init(bar_pfull(b), NSM);
+      mbar_init(bar_pfull(b), (EXPT == 3 ? 1 : CTAS) * SOFTMAX_WARPS);
       mbar_init(bar_pvdone(b), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     su32(tmem_ptr)),
-                 "r"(512)
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (CTAS == 1) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_ptr)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tmem_ptr)),
+                   "r"(512)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync_all();  // peer barriers initialised before any signal
+  else __syncthreads();
   tc_fence_after();
+  // leader-side copy of a barrier (remote for the peer CTA)
+  auto to_leader = [&](uint32_t bar) { return CTAS == 2 ? mapa_rank(bar, 0) : bar; };
+  auto arrive_tx = [&](uint32_t bar, uint32_t bytes) {
+    if (leader) mbar_expect_tx(bar, bytes * CTAS);
+    else mbar_arrive_cluster(to_leader(bar));
+  };
   const uint32_t tbase = *tmem_ptr;
   // TMEM: three S buffers (128 fp32 columns each) + O (128).  P_j (bf16x2,
   // 64 columns) overwrites the first half of S_j's buffer once the softmax
@@ -356,72 +480,108 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
   if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_expect_tx(bar_q, TILE_BYTES);
-      tma_load_3d(sQ, &map_q, bar_q, 0, g * p.G, a0);
-      tma_load_3d(sQ + ATOM_BYTES, &map_q, bar_q, 64, g * p.G, a0);
+      auto tma = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
+        if constexpr (CTAS == 1) tma_load_3d(dst, m, bar, c0, c1, c2);
+        else tma_load_3d_2sm(dst, m, bar, c0, c1, c2);
+      };
+      arrive_tx(bar_q, TILE_BYTES);
+      tma(sQ, &map_q, bar_q, 0, g * p.G, a0);
+      tma(sQ + ATOM_BYTES, &map_q, bar_q, 64, g * p.G, a0);
       int slot = 0;
       uint32_t phase = 0;
-      auto load = [&](const CUtensorMap* m, int j) {
+      // K_j: CTAS=1 the whole [128 keys][128 d] tile (two 64-d swizzle atoms);
+      // CTAS=2 keys [64r, 64r+64) of the block (MMA N half r), both d atoms.
+      int nloads = 0;
+      auto load_k = [&](int j) {
         mbar_wait(bar_empty(slot), phase ^ 1);
-        const uint32_t dst = sKV + slot * TILE_BYTES;
-        mbar_expect_tx(bar_full(slot), TILE_BYTES);
-        tma_load_3d(dst, m, bar_full(slot), 0, g, j * BLK_N);
-        tma_load_3d(dst + ATOM_BYTES, m, bar_full(slot), 64, g, j * BLK_N);
-        if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
+        const uint32_t dst = sKV + slot * SLOT;
+        if (EXPT == 4 && ++nloads > NSLOT) {  // probe: slots keep stale data
+          if (leader) mbar_arrive(bar_full(slot));
+          else mbar_arrive_cluster(to_leader(bar_full(slot)));
+          if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+          return;
+        }
+        arrive_tx(bar_full(slot), SLOT);
+        const int key0 = j * BLK_N + (int)crank * (BLK_N / CTAS);
+        tma(dst, &map_k, bar_full(slot), 0, g, key0);
+        tma(dst + SLOT / 2, &map_k, bar_full(slot), 64, g, key0);
+        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
       };
-      // same order the MMA warp consumes: K0, K1, V0, K2, V1, ...
-      load(&map_k, 0);
+      // V_j: CTAS=1 both 64-d atoms; CTAS=2 the d atom r (MMA N half r).
+      auto load_v = [&](int j) {
+        mbar_wait(bar_empty(slot), phase ^ 1);
+        const uint32_t dst = sKV + slot * SLOT;
+        if (EXPT == 4 && ++nloads > NSLOT) {
+          if (leader) mbar_arrive(bar_full(slot));
+          else mbar_arrive_cluster(to_leader(bar_full(slot)));
+          if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+          return;
+        }
+        arrive_tx(bar_full(slot), SLOT);
+        if constexpr (CTAS == 1) {
+          tma(dst, &map_v, bar_full(slot), 0, g, j * BLK_N);
+          tma(dst + ATOM_BYTES, &map_v, bar_full(slot), 64, g, j * BLK_N);
+        } else {
+          tma(dst, &map_v, bar_full(slot), 64 * (int)crank, g, j * BLK_N);
+        }
+        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+      };
+      // same order the MMA warp consumes: K0, K1, K2, V0, K3, V1, K4, ...
+      for (int j = 0; j < NSB && j < nb; ++j) load_k(j);
       for (int j = 0; j < nb; ++j) {
-        if (j + 1 < nb) load(&map_k, j + 1);
-        load(&map_v, j);
+        load_v(j);
+        if (j + NSB < nb) load_k(j + NSB);
       }
     }
   } else if (warp == MMA_WARP) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      constexpr uint32_t IDESC_S = idesc_bf16(false);
-      constexpr uint32_t IDESC_O = idesc_bf16(true);
+    if (lane == 0 && leader) {
+      constexpr uint32_t IDESC_S = idesc_bf16(false, TILE_M * CTAS);
+      constexpr uint32_t IDESC_O = idesc_bf16(true, TILE_M * CTAS);
+      constexpr int KATOM = SLOT / 2;  // bytes of one 64-d K atom in a slot
       mbar_wait(bar_q, 0);
       tc_fence_after();
       int slot = 0;
       uint32_t phase = 0;
+      // S_j goes into TMEM buffer j%3, which last held P_{j-3}.  S_j is issued
+      // right after PV_{j-3} (its reader) by this thread, and tcgen05.mma ops
+      // from one thread execute in issue order, so no wait is needed: two S
+      // blocks stay queued ahead of every PV while the softmax works.
       auto issue_s = [&](int j) {
         const int b = j % NSB;
-        // buffer b last held P_{j-3}: wait for its reader PV_{j-3}
-        if (j >= NSB) mbar_wait(bar_pvdone(b), ((j / NSB) - 1) & 1);
         mbar_wait(bar_full(slot), phase);
         tc_fence_after();
-        const uint32_t k_tile = sKV + slot * TILE_BYTES;
+        const uint32_t k_tile = sKV + slot * SLOT;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
-          tc_mma(tS(b), sdesc(sQ + off, 16, 1024), sdesc(k_tile + off, 16, 1024), IDESC_S,
-                 kk > 0);
+          const uint32_t koff = (kk & 3) * 32;
+          tc_mma_t<CTAS>(tS(b), sdesc(sQ + (kk >> 2) * ATOM_BYTES + koff, 16, 1024),
+                         sdesc(k_tile + (kk >> 2) * KATOM + koff, 16, 1024), IDESC_S, kk > 0);
         }
-        tc_commit(bar_empty(slot));
-        tc_commit(bar_sfull(b));
-        if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
+        tc_commit_t<CTAS>(bar_empty(slot));
+        tc_commit_t<CTAS>(bar_sfull(b));
+        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
       };
-      issue_s(0);
-      if (nb > 1) issue_s(1);
+      for (int j = 0; j < NSB && j < nb; ++j) issue_s(j);
       for (int j = 0; j < nb; ++j) {
         // O += P_j V_j
         const int b = j % NSB;
-        mbar_wait(bar_pfull(b), (j / NSB) & 1);
+        if constexpr (CTAS == 2) mbar_wait_cluster(bar_pfull(b), (j / NSB) & 1);
+        else mbar_wait(bar_pfull(b), (j / NSB) & 1);
         mbar_wait(bar_full(slot), phase);
         tc_fence_after();
-        const uint32_t v_tile = sKV + slot * TILE_BYTES;
+        const uint32_t v_tile = sKV + slot * SLOT;
 #pragma unroll
         for (int kk = 0; kk < BLK_N / 16; ++kk) {
           // A = P from TMEM (16 keys = 8 packed columns); B = V, MN-major,
           // K-step of 16 keys = 2 x 1024 B core-matrix groups
-          tc_mma_ts(tO, tS(b) + kk * 8, sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024), IDESC_O,
-                    (j > 0 || kk > 0) ? 1u : 0u);
+          tc_mma_ts_t<CTAS>(tO, tS(b) + kk * 8, sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024),
+                            IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        tc_commit(bar_empty(slot));
-        tc_commit(bar_pvdone(b));
-        if (++slot == KV_SLOTS) { slot = 0; phase ^= 1; }
-        if (j + 2 < nb) issue_s(j + 2);
+        tc_commit_t<CTAS>(bar_empty(slot));
+        tc_commit_t<CTAS>(bar_pvdone(b));
+        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+        if (j + NSB < nb) issue_s(j + NSB);
       }
     }
   } else {
@@ -438,7 +598,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
     const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
     const uint32_t lane_off = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF);
     const uint32_t lane_off_p = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF / 2);
-    float* xch = reinterpret_cast<float*>(gbase + Smem::XCH);  // [3][2][128]
+    float* xch = reinterpret_cast<float*>(gbase + SM::XCH);  // [3][2][128]
     float m_used = -INFINITY, l = 0.f;
     uint32_t r[HALF];
     for (int j = 0; j < nb; ++j) {
@@ -448,6 +608,37 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
       // warp-collective (.sync.aligned) tcgen05.ld
       __syncwarp();
       tc_fence_after();
+      if constexpr (EXPT == 2 || EXPT == 3 || EXPT == 4) {  // profiling aid: no softmax
+        tc_fence_before();
+        __syncwarp();
+        if (EXPT == 3 && !leader) continue;  // EXPT 3: leader does not wait for the peer
+        if (lane == 0) {
+          if constexpr (CTAS == 2) mbar_arrive_cluster(to_leader(bar_pfull(b)));
+          else mbar_arrive(bar_pfull(b));
+        }
+        continue;
+      }
+      if constexpr (EXPT == 1) {  // profiling aid: TMEM S load + P store only
+#pragma unroll
+        for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS(b) + lane_off + c * 32, r + c * 32);
+#pragma unroll
+        for (int c = 0; c < HALF / 32; ++c) tmem_wait_ld32(r + c * 32);
+        uint32_t pk[HALF / 2];
+#pragma unroll
+        for (int c = 0; c < HALF / 2; ++c) pk[c] = r[2 * c] ^ r[2 * c + 1];
+        asm volatile("bar.sync 1, %0;" ::"n"(NSM) : "memory");
+        __syncwarp();
+#pragma unroll
+        for (int c = 0; c < HALF / 64; ++c) tmem_st32(tS(b) + lane_off_p + c * 32, pk + c * 32);
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if constexpr (CTAS == 2) mbar_arrive_cluster(to_leader(bar_pfull(b)));
+          else mbar_arrive(bar_pfull(b));
+        }
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS(b) + lane_off + c * 32, r + c * 32);
 #pragma unroll
@@ -530,7 +721,11 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
         tmem_wait_st();
       }
       tc_fence_before();
-      mbar_arrive(bar_pfull(b));
+      __syncwarp();  // every lane's P store + O rescale precede the warp's arrive
+      if (lane == 0) {
+          if constexpr (CTAS == 2) mbar_arrive_cluster(to_leader(bar_pfull(b)));
+          else mbar_arrive(bar_pfull(b));
+        }
     }
     // epilogue: combine the two partial row sums, O[:, half] / l -> global
     if constexpr (NSPLIT > 1) {
@@ -575,11 +770,16 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CTAS == 2) cluster_sync_all();  // both CTAs done with TMEM and barriers
+  else __syncthreads();
   if (warp == MMA_WARP) {
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
-                 : "memory");
+    if constexpr (CTAS == 1)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                   : "memory");
   }
 }
 
@@ -637,8 +837,9 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   if ((rc = make_map(&mq, q, (uint64_t)Hq, (uint64_t)A, HD * 2, (uint64_t)Hq * HD * 2,
                      (uint32_t)G, (uint32_t)(TILE_M / G))))
     return rc;
+  const int kbox = (getenv("CT_TC_CTAS") && atoi(getenv("CT_TC_CTAS")) == 2) ? BLK_N / 2 : BLK_N;
   if ((rc = make_map(&mk, k_cache, (uint64_t)Hkv, (uint64_t)n_ctx, HD * 2,
-                     (uint64_t)cache_row_stride * 2, 1, BLK_N)))
+                     (uint64_t)cache_row_stride * 2, 1, (uint32_t)kbox)))
     return rc;
   if ((rc = make_map(&mv, v_cache, (uint64_t)Hkv, (uint64_t)n_ctx, HD * 2,
                      (uint64_t)cache_row_stride * 2, 1, BLK_N)))
@@ -657,18 +858,49 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   prm.scale_log2 = (float)(scale * 1.4426950408889634);
   prm.lazy_thresh = LAZY_THRESH;
   if (const char* e = getenv("CT_TC_LAZY")) prm.lazy_thresh = (float)atof(e);
-  const size_t smem = Smem::TOTAL + 1024;
-  int split = 2;
-  if (const char* e = getenv("CT_TC_SPLIT")) split = atoi(e);
+  // Single-CTA tiles by default.  CT_TC_CTAS=2 selects the CTA-pair kernel
+  // (cta_group::2, MMA M = 256, half of every K/V tile per SM): correct and it
+  // halves L2->SM traffic, but measured 40 % slower (its 2-SM TMA pipeline
+  // starves the MMA; profiles/round1_attention_variants.md).  CT_TC_EXPT /
+  // CT_TC_POLY are profiling aids.
+  int ctas = 1;
+  if (const char* e = getenv("CT_TC_CTAS")) ctas = atoi(e) == 2 ? 2 : 1;
   uint32_t poly = 0;
   if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
-  auto kern = split == 4 ? attention_tc_kernel<4, 0> : split == 1 ? attention_tc_kernel<1, 0>
-            : poly == 0x22 ? attention_tc_kernel<2, 0x22> : poly == 0x01 ? attention_tc_kernel<2, 0x01>
-            : poly == 0x55 ? attention_tc_kernel<2, 0x55> : attention_tc_kernel<2, 0>;
-  const int threads = 32 * (4 * (split == 4 ? 4 : split == 1 ? 1 : 2) + 2);
+  int expt = 0;
+  if (const char* e = getenv("CT_TC_EXPT")) expt = atoi(e);
+  using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Params);
+  KernFn kern;
+  if (ctas == 2)
+    kern = expt == 1 ? attention_tc_kernel<2, 0, 1, 2> : expt == 2 ? attention_tc_kernel<2, 0, 2, 2>
+         : expt == 3 ? attention_tc_kernel<2, 0, 3, 2> : expt == 4 ? attention_tc_kernel<2, 0, 4, 2>
+         : poly == 0x22 ? attention_tc_kernel<2, 0x22, 0, 2> : attention_tc_kernel<2, 0, 0, 2>;
+  else
+    kern = expt == 1 ? attention_tc_kernel<2, 0, 1, 1> : expt == 2 ? attention_tc_kernel<2, 0, 2, 1>
+         : expt == 4 ? attention_tc_kernel<2, 0, 4, 1>
+         : poly == 0x22 ? attention_tc_kernel<2, 0x22, 0, 1> : attention_tc_kernel<2, 0, 0, 1>;
+  const size_t smem = (ctas == 2 ? Smem<2>::TOTAL : Smem<1>::TOTAL) + 1024;
+  const int threads = 32 * (4 * 2 + 2);
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const unsigned grid = (unsigned)(prm.n_qblocks * Hkv);
-  kern<<<grid, threads, smem, st>>>(mq, mk, mv, prm);
+  const int units = (prm.n_qblocks + ctas - 1) / ctas;
+  const unsigned grid = (unsigned)(units * Hkv * ctas);
+  if (ctas == 1) {
+    kern<<<grid, threads, smem, st>>>(mq, mk, mv, prm);
+  } else {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    CT_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, prm));
+  }
   return check_launch("attention_tc_kernel");
 }
 
