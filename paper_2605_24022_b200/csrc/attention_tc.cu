@@ -18,6 +18,7 @@
 #include "common.cuh"
 
 #include <cuda.h>
+#include <type_traits>
 #include <cudaTypedefs.h>
 
 namespace ct {
@@ -783,6 +784,290 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Ping-pong kernel: two 128-row query tiles (X = 0, 1: adjacent query blocks
+// of one kv head) per CTA share every K/V tile.  TMEM = S_0 | S_1 | O_0 | O_1
+// (128 columns each; P_X aliases the first half of S_X).  One softmax thread
+// per tile row (warps 0-3 tile 0, warps 4-7 tile 1, so every SMSP runs one
+// warp of each tile), and the MMA order
+//     S_0(0) S_1(0) | PV_0(j) S_0(j+1) PV_1(j) S_1(j+1) | ...
+// keeps one tile's MMAs in the pipe while the other tile's softmax runs, so
+// the two softmax warps of an SMSP are out of phase and the exp2 (MUFU) work
+// of one overlaps the TMEM load / row max / P store of the other.  K/V bytes
+// per FLOP from L2 halve versus the single-tile kernel.
+// ---------------------------------------------------------------------------
+struct SmemPP {
+  static constexpr int SLOTS = 4;
+  static constexpr int Q = 0;                        // two Q tiles
+  static constexpr int KV = Q + 2 * TILE_BYTES;
+  static constexpr int BAR = KV + SLOTS * TILE_BYTES;
+  // q, full[4], empty[4], per tile: sfull, pfull, pvdone
+  static constexpr int NBAR = 1 + 2 * SLOTS + 6;
+  static constexpr int TMEM_PTR = BAR + NBAR * 8;
+  static constexpr int TOTAL = TMEM_PTR + 16;
+};
+
+template <uint32_t POLY_MASK>
+__global__ void __launch_bounds__(32 * 10, 1)
+attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
+                    const __grid_constant__ CUtensorMap map_k,
+                    const __grid_constant__ CUtensorMap map_v, const Params p) {
+  constexpr int TMA_WARP = 8, MMA_WARP = 9;
+  constexpr int NSLOT = SmemPP::SLOTS;
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = su32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const uint32_t sQ = base + SmemPP::Q, sKV = base + SmemPP::KV;
+  const uint32_t bar0 = base + SmemPP::BAR;
+  const uint32_t bar_q = bar0;
+  auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };
+  auto bar_empty = [&](int s) { return bar0 + (1 + NSLOT + s) * 8; };
+  constexpr int B2 = 1 + 2 * NSLOT;
+  auto bar_sfull = [&](int x) { return bar0 + (B2 + x) * 8; };
+  auto bar_pfull = [&](int x) { return bar0 + (B2 + 2 + x) * 8; };
+  auto bar_pvdone = [&](int x) { return bar0 + (B2 + 4 + x) * 8; };
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + SmemPP::TMEM_PTR);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // longest units first; unit = two adjacent query blocks of kv head g
+  const int n_units = (p.n_qblocks + 1) / 2;
+  const int qb0 = (n_units - 1 - (int)(blockIdx.x / p.Hkv)) * 2;
+  const int g = blockIdx.x % p.Hkv;
+  int maxpos = 0;
+  for (int i = 0; i < 2 * p.QB; ++i) {
+    const int a = qb0 * p.QB + i;
+    if (a < p.A) maxpos = max(maxpos, __ldg(p.qpos + a));
+  }
+  maxpos = min(maxpos, p.n_ctx - 1);
+  const int nb = maxpos / BLK_N + 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar_q, 1);
+    for (int s = 0; s < NSLOT; ++s) {
+      mbar_init(bar_full(s), 1);
+      mbar_init(bar_empty(s), 1);
+    }
+    for (int x = 0; x < 2; ++x) {
+      mbar_init(bar_sfull(x), 1);
+      mbar_init(bar_pfull(x), 4);  // one elected arrive per softmax warp of the tile
+      mbar_init(bar_pvdone(x), 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     su32(tmem_ptr)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tbase = *tmem_ptr;
+  auto tS = [&](int x) { return tbase + (uint32_t)(x * 128); };
+  auto tO = [&](int x) { return tbase + 256u + (uint32_t)(x * 128); };
+
+  if (warp == TMA_WARP) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      mbar_expect_tx(bar_q, 2 * TILE_BYTES);
+      for (int x = 0; x < 2; ++x) {
+        const int a0 = (qb0 + x) * p.QB;
+        tma_load_3d(sQ + x * TILE_BYTES, &map_q, bar_q, 0, g * p.G, a0);
+        tma_load_3d(sQ + x * TILE_BYTES + ATOM_BYTES, &map_q, bar_q, 64, g * p.G, a0);
+      }
+      int slot = 0;
+      uint32_t phase = 0;
+      auto load = [&](const CUtensorMap* m, int j) {
+        mbar_wait(bar_empty(slot), phase ^ 1);
+        const uint32_t dst = sKV + slot * TILE_BYTES;
+        mbar_expect_tx(bar_full(slot), TILE_BYTES);
+        tma_load_3d(dst, m, bar_full(slot), 0, g, j * BLK_N);
+        tma_load_3d(dst + ATOM_BYTES, m, bar_full(slot), 64, g, j * BLK_N);
+        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
+      };
+      for (int j = 0; j < nb; ++j) {  // consumption order: K0 V0 K1 V1 ...
+        load(&map_k, j);
+        load(&map_v, j);
+      }
+    }
+  } else if (warp == MMA_WARP) {
+    // ------------------------------------------------------------ MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t IDESC_S = idesc_bf16(false);
+      constexpr uint32_t IDESC_O = idesc_bf16(true);
+      mbar_wait(bar_q, 0);
+      tc_fence_after();
+      // K_j lives in slot (2j) % NSLOT, V_j in (2j+1) % NSLOT
+      auto slot_of = [&](int i) { return i % NSLOT; };
+      auto par_of = [&](int i) { return (uint32_t)((i / NSLOT) & 1); };
+      auto issue_s = [&](int x, int j) {
+        const int i = 2 * j, s = slot_of(i);
+        if (x == 0) {
+          mbar_wait(bar_full(s), par_of(i));
+          tc_fence_after();
+        }
+        const uint32_t k_tile = sKV + s * TILE_BYTES;
+        const uint32_t q_tile = sQ + x * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
+          tc_mma(tS(x), sdesc(q_tile + off, 16, 1024), sdesc(k_tile + off, 16, 1024), IDESC_S,
+                 kk > 0);
+        }
+        if (x == 1) tc_commit(bar_empty(s));
+        tc_commit(bar_sfull(x));
+      };
+      auto issue_pv = [&](int x, int j) {
+        const int i = 2 * j + 1, s = slot_of(i);
+        mbar_wait(bar_pfull(x), (uint32_t)(j & 1));
+        if (x == 0) mbar_wait(bar_full(s), par_of(i));
+        tc_fence_after();
+        const uint32_t v_tile = sKV + s * TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < BLK_N / 16; ++kk)
+          tc_mma_ts(tO(x), tS(x) + kk * 8, sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024), IDESC_O,
+                    (j > 0 || kk > 0) ? 1u : 0u);
+        if (x == 1) tc_commit(bar_empty(s));
+        tc_commit(bar_pvdone(x));
+      };
+      issue_s(0, 0);
+      issue_s(1, 0);
+      for (int j = 0; j < nb; ++j) {
+        // S_x(j+1) overwrites the columns PV_x(j) reads as P: same thread,
+        // in-order tcgen05.mma pipe, so it is issued right behind it
+        issue_pv(0, j);
+        if (j + 1 < nb) issue_s(0, j + 1);
+        issue_pv(1, j);
+        if (j + 1 < nb) issue_s(1, j + 1);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const int x = warp >> 2;                  // tile
+    const int m = (warp & 3) * 32 + lane;     // TMEM lane / tile row
+    const int qi = m / p.G, hj = m % p.G;
+    const int a = (qb0 + x) * p.QB + qi;
+    const bool valid = a < p.A;
+    const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
+    const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+    float m_used = -INFINITY, l = 0.f;
+    uint32_t r[BLK_N];
+    for (int j = 0; j < nb; ++j) {
+      mbar_wait(bar_sfull(x), (uint32_t)(j & 1));
+      __syncwarp();
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < BLK_N / 32; ++c) tmem_ld32(tS(x) + lane_off + c * 32, r + c * 32);
+#pragma unroll
+      for (int c = 0; c < BLK_N / 32; ++c) tmem_wait_ld32(r + c * 32);
+      const int kbase = j * BLK_N;
+      const bool need_mask = kbase + BLK_N - 1 > pos;
+      if (need_mask) {
+#pragma unroll
+        for (int c = 0; c < BLK_N; ++c)
+          if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
+      }
+      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < BLK_N; c += 8) {
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
+      }
+      const float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
+      const float m_new = fmaxf(m_used, mx);
+      const bool grow = m_new > m_used + p.lazy_thresh;
+      const bool any_grow = __any_sync(0xffffffffu, grow);
+      const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
+      if (grow) m_used = m_new;
+      const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
+      const uint64_t nm2 = pk2(-m_used, -m_used);
+      uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
+      // P_j (bf16x2) -> TMEM columns [0, 64) of S_x, 32 keys per store
+      auto chunk = [&](auto cc) {
+        constexpr int c = decltype(cc)::value;
+        uint32_t pk[16];
+        if (need_mask)
+          softmax_chunks<32, 0u>(r + c * 32, sc2, nm2, acc2, pk);
+        else
+          softmax_chunks<32, (POLY_MASK >> (4 * c)) & 0xFu>(r + c * 32, sc2, nm2, acc2, pk);
+        tmem_st16(tS(x) + lane_off + c * 16, pk);
+      };
+      chunk(std::integral_constant<int, 0>{});
+      chunk(std::integral_constant<int, 1>{});
+      chunk(std::integral_constant<int, 2>{});
+      chunk(std::integral_constant<int, 3>{});
+      {
+        float s0, s1, s2, s3;
+        upk2(acc2[0], s0, s1);
+        upk2(acc2[1], s2, s3);
+        l = l * corr + ((s0 + s1) + (s2 + s3));
+      }
+      tmem_wait_st();
+      if (any_grow && j > 0) {
+        // O_x *= corr once PV_x(j-1) has landed (warp-uniform branch)
+        mbar_wait(bar_pvdone(x), (uint32_t)((j - 1) & 1));
+        __syncwarp();
+        tc_fence_after();
+#pragma unroll 1
+        for (int c = 0; c < HD / 32; ++c) {
+          uint32_t o[32];
+          tmem_ld32(tO(x) + lane_off + c * 32, o);
+          tmem_wait_ld32(o);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+          tmem_st32(tO(x) + lane_off + c * 32, o);
+        }
+        tmem_wait_st();
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar_pfull(x));
+    }
+    mbar_wait(bar_pvdone(x), (uint32_t)((nb - 1) & 1));
+    __syncwarp();
+    tc_fence_after();
+    const float inv = valid ? 1.f / l : 0.f;
+    const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD;
+#pragma unroll 1
+    for (int c = 0; c < HD / 32; ++c) {
+      uint32_t o[32];
+      tmem_ld32(tO(x) + lane_off + c * 32, o);
+      tmem_wait_ld32(o);
+      if (valid) {
+        if (p.out_f32) {
+          float4* dst = reinterpret_cast<float4*>(p.out_f32 + orow + c * 32);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+        } else {
+          uint4* dst = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            uint4 v;
+            v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
+            v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
+            v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
+            v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
+            dst[e] = v;
+          }
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
+                 : "memory");
+  }
+}
+
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
 
 static EncodeFn encode_fn() {
@@ -865,12 +1150,31 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   // CT_TC_POLY are profiling aids.
   int ctas = 1;
   if (const char* e = getenv("CT_TC_CTAS")) ctas = atoi(e) == 2 ? 2 : 1;
-  uint32_t poly = 0;
+  // FMA-pipe exp2 for a quarter of the scores (8-column group 2 of every 32)
+  // measured best for the ping-pong kernel (profiles/round1_attention_variants.md)
+  uint32_t poly = 0x4444;
   if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
   int expt = 0;
   if (const char* e = getenv("CT_TC_EXPT")) expt = atoi(e);
   using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Params);
   KernFn kern;
+  int pp = 1;
+  if (const char* e = getenv("CT_TC_PP")) pp = atoi(e);
+  if (pp && ctas == 1 && expt == 0) {
+    KernFn kp = poly == 0x3333 ? attention_pp_kernel<0x3333u>
+              : poly == 0x7777 ? attention_pp_kernel<0x7777u>
+              : poly == 0xFFFF ? attention_pp_kernel<0xFFFFu>
+              : poly == 0x4444 ? attention_pp_kernel<0x4444u>
+              : poly == 0x0202 ? attention_pp_kernel<0x0202u>
+              : poly == 0x5555 ? attention_pp_kernel<0x5555u>
+              : poly == 0x1111 ? attention_pp_kernel<0x1111u>
+              : poly == 0x2222 ? attention_pp_kernel<0x2222u> : attention_pp_kernel<0u>;
+    const size_t smem_pp = SmemPP::TOTAL + 1024;
+    CT_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pp));
+    const unsigned grid_pp = (unsigned)(((prm.n_qblocks + 1) / 2) * Hkv);
+    kp<<<grid_pp, 320, smem_pp, st>>>(mq, mk, mv, prm);
+    return check_launch("attention_pp_kernel");
+  }
   if (ctas == 2)
     kern = expt == 1 ? attention_tc_kernel<2, 0, 1, 2> : expt == 2 ? attention_tc_kernel<2, 0, 2, 2>
          : expt == 3 ? attention_tc_kernel<2, 0, 3, 2> : expt == 4 ? attention_tc_kernel<2, 0, 4, 2>
