@@ -185,11 +185,14 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
         if hook is not None:
             hook(l, "start")
         torch.mm(buf.x, w["wqkv"], out=buf.qkv)
+        tq = timer.start("qkv") if timer is not None else None
         _lib.check(lib.ct_qkv_rope_scatter(
             _dev.ptr(buf.qkv), buf.qkv.shape[1], dtc, _dev.ptr(positions), a, hq, hkv, d,
             params.pairing_code, _dev.ptr(table), _dev.ptr(buf.q), dtc, _dev.ptr(kc),
             _dev.ptr(vc), dtc, hkv * d, _dev.ptr(k_raw_out[l]) if k_raw_out else None, st),
             "ct_qkv_rope_scatter")
+        if timer is not None:
+            timer.stop("qkv", tq)
         if hook is not None:
             hook(l, "recomputed")
         if reuse is not None:
