@@ -28,6 +28,7 @@ _LAZY = {
     "AttentionRecord": "prefill", "attention_deviation": "prefill",
     "STRATEGIES": "experiments", "strategy_ranking": "experiments",
     "effective_ratio": "experiments", "run_selection_experiment": "experiments",
+    "FrequencyTokenRanker": "estimators", "RatioCalibrator": "estimators",
 }
 
 
