@@ -403,7 +403,13 @@ struct Fft2Cfg {
   static constexpr size_t SIG_BYTES = (size_t)NG * SIGPAD * sizeof(cpx<T>);
   static constexpr size_t TILE_BYTES = (size_t)N * TW * sizeof(IN);
   static constexpr size_t ACC_BYTES = (size_t)N * sizeof(double);
-  static constexpr size_t SMEM = SIG_BYTES + TILE_BYTES + ACC_BYTES;
+  // twiddle tables: f2 [16 r][16 (t&15)], i2 [16 r][R3 (t%R3)], and (when it
+  // fits) the per-thread table T3 [16 r][GT t] = W_N^{t r} for f3 / i3
+  static constexpr size_t T2_BYTES = (size_t)16 * (16 + R3) * sizeof(cpx<T>);
+  static constexpr size_t T3_BYTES = (size_t)16 * GT * sizeof(cpx<T>);
+  static constexpr size_t BASE = SIG_BYTES + TILE_BYTES + ACC_BYTES + T2_BYTES;
+  static constexpr bool USE_T3 = BASE + T3_BYTES <= 227 * 1024;
+  static constexpr size_t SMEM = BASE + (USE_T3 ? T3_BYTES : 0);
   static_assert(NG * N == 8192, "8192 points in flight per CTA");
 };
 
@@ -444,6 +450,27 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
   // per-token energy of the CTA's signals, summed group by group in a fixed
   // order (registers hold the FFT; a per-thread f64 accumulator would spill)
   double* acc = reinterpret_cast<double*>(smem_raw + Cfg::SIG_BYTES + Cfg::TILE_BYTES);
+  cpx<T>* t2f = reinterpret_cast<cpx<T>*>(smem_raw + Cfg::SIG_BYTES + Cfg::TILE_BYTES +
+                                          Cfg::ACC_BYTES);
+  cpx<T>* t2i = t2f + 16 * 16;
+  cpx<T>* t3 = t2i + 16 * R3;
+  // tables from the N-point table (exact entries: no products)
+  for (int q = threadIdx.x; q < 16 * 16; q += FFT2_THREADS) {
+    const int r = q / 16, u = q % 16;
+    t2f[q] = tw[(u * r * R3) & (N - 1)];
+  }
+  for (int q = threadIdx.x; q < 16 * R3; q += FFT2_THREADS) {
+    const int r = q / R3, u = q % R3;
+    cpx<T> w = tw[(u * r * 16) & (N - 1)];
+    w.y = -w.y;
+    t2i[q] = w;
+  }
+  if constexpr (Cfg::USE_T3) {
+    for (int q = threadIdx.x; q < 16 * GT; q += FFT2_THREADS) {
+      const int r = q / GT, u = q % GT;
+      t3[q] = tw[(u * r) & (N - 1)];
+    }
+  }
 
   const int g = threadIdx.x / GT, t = threadIdx.x % GT;
   cpx<T>* sig = sigall + g * Cfg::SIGPAD;
@@ -481,7 +508,8 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
     // ---- f2: radix 16, Ns = 16
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = sig[sp16<T>(t + GT * r)];
-    twiddle<16, false, N>(v, tw, (t & 15) * R3);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], t2f[r * 16 + (t & 15)]);
     dft16<false>(v);
     group_sync<GT>(g);
 #pragma unroll
@@ -494,7 +522,17 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
       cpx<T>* w = v + q * R3;
 #pragma unroll
       for (int r = 0; r < R3; ++r) w[r] = sig[sp16<T>(j + NR3 * r)];
-      twiddle<R3, false, N>(w, tw, j);
+      if constexpr (Cfg::USE_T3) {
+        // W_N^{(t + q GT) r} = W_N^{t r} W_N^{q GT r}
+#pragma unroll
+        for (int r = 1; r < R3; ++r) {
+          cpx<T> tr = t3[r * GT + t];
+          if (q > 0) tr = cmul(tr, tw[(q * GT * r) & (N - 1)]);
+          w[r] = cmul(w[r], tr);
+        }
+      } else {
+        twiddle<R3, false, N>(w, tw, j);
+      }
       dft_r<R3, false>(w);
 #pragma unroll
       for (int r = 0; r < R3; ++r) {
@@ -515,7 +553,8 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
     // ---- i2: inverse radix 16, Ns = R3
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = sig[sp16<T>(t + GT * r)];
-    twiddle<16, true, N>(v, tw, (t % R3) * 16);
+#pragma unroll
+    for (int r = 1; r < 16; ++r) v[r] = cmul(v[r], t2i[r * R3 + (t % R3)]);
     dft16<true>(v);
     group_sync<GT>(g);
 #pragma unroll
@@ -524,7 +563,16 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
     // ---- i3: inverse radix 16, Ns = N/16 -> token t + GT r in v[r]
 #pragma unroll
     for (int r = 0; r < 16; ++r) v[r] = sig[sp16<T>(t + GT * r)];
-    twiddle<16, true, N>(v, tw, t);
+    if constexpr (Cfg::USE_T3) {
+#pragma unroll
+      for (int r = 1; r < 16; ++r) {
+        cpx<T> w = t3[r * GT + t];
+        w.y = -w.y;
+        v[r] = cmul(v[r], w);
+      }
+    } else {
+      twiddle<16, true, N>(v, tw, t);
+    }
     dft16<true>(v);
     double e[16];
 #pragma unroll
@@ -799,7 +847,10 @@ static int launch_fft(int logn, const void* k, const void* v, int L, int C, int 
       case 9: return launch_fft2_t<T, IN, 2>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
       case 10: return launch_fft2_t<T, IN, 4>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
       case 11: return launch_fft2_t<T, IN, 8>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
-      case 12: return launch_fft2_t<T, IN, 16>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+      case 12:  // f64 with f32 inputs does not fit one CTA at N = 4096: v1 below
+        if (Fft2Cfg<T, IN, 16>::SMEM <= 227 * 1024)
+          return launch_fft2_t<T, IN, 16>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+        break;
       default: break;
     }
   }
