@@ -577,13 +577,19 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
     double e[16];
 #pragma unroll
     for (int r = 0; r < 16; ++r) e[r] = (double)(v[r].x * v[r].x + v[r].y * v[r].y);
-    cp_async_wait_all();  // next tile landed (its barrier is the last one below)
-    for (int q = 0; q < NG; ++q) {
-      if (g == q) {
+    // energies -> the group's (now free) exchange buffer, then one barrier and
+    // acc[n] += e_0[n] + e_1[n] + ... in group order (fixed, deterministic)
+    group_sync<GT>(g);
+    double* eb = reinterpret_cast<double*>(sig);
 #pragma unroll
-        for (int r = 0; r < 16; ++r) acc[t + GT * r] += e[r];
-      }
-      __syncthreads();
+    for (int r = 0; r < 16; ++r) eb[t + GT * r] = e[r];
+    cp_async_wait_all();  // next tile landed; the barrier publishes it too
+    __syncthreads();
+    for (int n = threadIdx.x; n < N; n += FFT2_THREADS) {
+      double a_n = acc[n];
+#pragma unroll
+      for (int q = 0; q < NG; ++q) a_n += reinterpret_cast<const double*>(sigall + q * Cfg::SIGPAD)[n];
+      acc[n] = a_n;
     }
   }
   const double inv_n2 = 1.0 / ((double)N * (double)N);
