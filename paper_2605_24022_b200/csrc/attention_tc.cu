@@ -807,7 +807,7 @@ struct SmemPP {
   static constexpr int TOTAL = TMEM_PTR + 16;
 };
 
-template <uint32_t POLY_MASK>
+template <uint32_t POLY_MASK, int SCHED = 1>
 __global__ void __launch_bounds__(32 * 10, 1)
 attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
@@ -987,19 +987,65 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
       const uint64_t nm2 = pk2(-m_used, -m_used);
       uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
       // P_j (bf16x2) -> TMEM columns [0, 64) of S_x, 32 keys per store
-      auto chunk = [&](auto cc) {
-        constexpr int c = decltype(cc)::value;
-        uint32_t pk[16];
-        if (need_mask)
-          softmax_chunks<32, 0u>(r + c * 32, sc2, nm2, acc2, pk);
-        else
-          softmax_chunks<32, (POLY_MASK >> (4 * c)) & 0xFu>(r + c * 32, sc2, nm2, acc2, pk);
-        tmem_st16(tS(x) + lane_off + c * 16, pk);
-      };
-      chunk(std::integral_constant<int, 0>{});
-      chunk(std::integral_constant<int, 1>{});
-      chunk(std::integral_constant<int, 2>{});
-      chunk(std::integral_constant<int, 3>{});
+      if constexpr (SCHED == 0) {
+        auto chunk = [&](auto cc) {
+          constexpr int c = decltype(cc)::value;
+          uint32_t pk[16];
+          if (need_mask)
+            softmax_chunks<32, 0u>(r + c * 32, sc2, nm2, acc2, pk);
+          else
+            softmax_chunks<32, (POLY_MASK >> (4 * c)) & 0xFu>(r + c * 32, sc2, nm2, acc2, pk);
+          tmem_st16(tS(x) + lane_off + c * 16, pk);
+        };
+        chunk(std::integral_constant<int, 0>{});
+        chunk(std::integral_constant<int, 1>{});
+        chunk(std::integral_constant<int, 2>{});
+        chunk(std::integral_constant<int, 3>{});
+      } else {
+        // phased, per half block (64 keys): the FFMA2 arguments, then the exp2
+        // run back to back (MUFU / polynomial), then packing + row sums + TMEM
+        // stores, so one warp keeps the MUFU pipe fed without per-chunk chains
+#pragma unroll
+        for (int hb = 0; hb < 2; ++hb) {
+          uint32_t* rh = r + hb * 64;
+#pragma unroll
+          for (int c = 0; c < 64; c += 2) {
+            const uint64_t a2 = ffma2(pk2(__uint_as_float(rh[c]), __uint_as_float(rh[c + 1])), sc2, nm2);
+            float a, b;
+            upk2(a2, a, b);
+            rh[c] = __float_as_uint(a);
+            rh[c + 1] = __float_as_uint(b);
+          }
+          if (need_mask) {
+#pragma unroll
+            for (int c = 0; c < 64; ++c) rh[c] = __float_as_uint(ex2(__uint_as_float(rh[c])));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 64; c += 2) {
+              if ((POLY_MASK >> ((hb * 64 + c) / 8)) & 1) {
+                uint32_t o0, o1;
+                exp2_poly2(pk2(__uint_as_float(rh[c]), __uint_as_float(rh[c + 1])), o0, o1);
+                rh[c] = o0;
+                rh[c + 1] = o1;
+              } else {
+                rh[c] = __float_as_uint(ex2(__uint_as_float(rh[c])));
+                rh[c + 1] = __float_as_uint(ex2(__uint_as_float(rh[c + 1])));
+              }
+            }
+          }
+#pragma unroll
+          for (int c = 0; c < 2; ++c) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+              const uint32_t e0 = rh[c * 32 + 2 * t], e1 = rh[c * 32 + 2 * t + 1];
+              acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e0 | ((uint64_t)e1 << 32));
+              pk[t] = pack_bf16(__uint_as_float(e0), __uint_as_float(e1));
+            }
+            tmem_st16(tS(x) + lane_off + (hb * 2 + c) * 16, pk);
+          }
+        }
+      }
       {
         float s0, s1, s2, s3;
         upk2(acc2[0], s0, s1);
@@ -1150,9 +1196,9 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   // CT_TC_POLY are profiling aids.
   int ctas = 1;
   if (const char* e = getenv("CT_TC_CTAS")) ctas = atoi(e) == 2 ? 2 : 1;
-  // FMA-pipe exp2 for a quarter of the scores (8-column group 2 of every 32)
-  // measured best for the ping-pong kernel (profiles/round1_attention_variants.md)
-  uint32_t poly = 0x4444;
+  // exp2 on MUFU only: with the phased softmax the FMA-pipe polynomial no
+  // longer pays (profiles/round1_attention_variants.md); CT_TC_POLY selects it
+  uint32_t poly = 0;
   if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
   int expt = 0;
   if (const char* e = getenv("CT_TC_EXPT")) expt = atoi(e);
@@ -1161,7 +1207,10 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   int pp = 1;
   if (const char* e = getenv("CT_TC_PP")) pp = atoi(e);
   if (pp && ctas == 1 && expt == 0) {
-    KernFn kp = poly == 0x3333 ? attention_pp_kernel<0x3333u>
+    int sched = 1;
+    if (const char* e = getenv("CT_TC_SCHED")) sched = atoi(e);
+    KernFn kp = sched == 0 ? (poly == 0x4444 ? attention_pp_kernel<0x4444u, 0> : attention_pp_kernel<0u, 0>)
+              : poly == 0x3333 ? attention_pp_kernel<0x3333u>
               : poly == 0x7777 ? attention_pp_kernel<0x7777u>
               : poly == 0xFFFF ? attention_pp_kernel<0xFFFFu>
               : poly == 0x4444 ? attention_pp_kernel<0x4444u>
