@@ -39,6 +39,9 @@ def _run(q, pos, k, v, hq, hkv, out_dtype=torch.bfloat16):
     (1000, 8, 8, 5000, True),     # MHA (G=1), 8 q-blocks
     (77, 16, 2, 3001, False),     # G=8, unsorted positions
     (4992, 32, 8, 32832, True),   # config-2 layer shape (selected + suffix rows)
+    (1, 32, 8, 1, True),          # one query, one key
+    (5, 64, 4, 700, True),        # G=16 (8 queries per tile), odd tile count
+    (129, 8, 8, 129, True),       # MHA, A = n_ctx = 129 (dense causal, ragged)
 ])
 def test_tc_attention_matches_torch(a, hq, hkv, n, sorted_pos):
     if not torch.cuda.is_available():
