@@ -74,6 +74,15 @@ def ncu_traffic(kernel: str, config: str):
     return None if entry is None else entry["bytes"]
 
 
+def ncu_field(kernel: str, field: str, config: str):
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if config != "cfg2" or not p.exists():
+        return None
+    entry = json.loads(p.read_text()).get(kernel) or {}
+    v = entry.get(field)
+    return None if v is None else v / 100.0
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -444,6 +453,11 @@ def run_ours(args, rank, world, local_rank):
                 "achieved_tflops": sc_flops / (sc64 * 1e-3) / 1e12,
                 "fp64_peak_tflops": fp64_peak,
                 "fp64_frac": sc_flops / (sc64 * 1e-3) / 1e12 / fp64_peak,
+                "fp64_pipe_busy_ncu": ncu_field("fft2_energy_kernel_f64", "fp64_pipe_pct",
+                                                args.config),
+                "note": "exact (f64) mode is FP64-pipe bound: achieved/peak counts split-radix "
+                        "flops (a DADD is 1 flop), the pipe-busy figure is from the committed "
+                        "ncu capture",
                 "traffic": ncu_traffic("fft2_energy_kernel_f64", args.config)},
             "scorer_f32_per_request": {
                 "ms": sc32, "hbm_gbs": scorer_bytes / (sc32 * 1e-3) / 1e9,
