@@ -797,7 +797,7 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
 // per FLOP from L2 halve versus the single-tile kernel.
 // ---------------------------------------------------------------------------
 struct SmemPP {
-  static constexpr int SLOTS = 4;
+  static constexpr int SLOTS = 5;
   static constexpr int Q = 0;                        // two Q tiles
   static constexpr int KV = Q + 2 * TILE_BYTES;
   static constexpr int BAR = KV + SLOTS * TILE_BYTES;
@@ -1016,7 +1016,10 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
             rh[c] = __float_as_uint(a);
             rh[c + 1] = __float_as_uint(b);
           }
-          if (need_mask) {
+          if (SCHED == 3) {  // timing probe (wrong values): exp2 replaced by an FMUL
+#pragma unroll
+            for (int c = 0; c < 64; ++c) rh[c] = __float_as_uint(__uint_as_float(rh[c]) * 0.5f);
+          } else if (need_mask) {
 #pragma unroll
             for (int c = 0; c < 64; ++c) rh[c] = __float_as_uint(ex2(__uint_as_float(rh[c])));
           } else {
@@ -1210,6 +1213,7 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
     int sched = 1;
     if (const char* e = getenv("CT_TC_SCHED")) sched = atoi(e);
     KernFn kp = sched == 0 ? (poly == 0x4444 ? attention_pp_kernel<0x4444u, 0> : attention_pp_kernel<0u, 0>)
+              : sched == 3 ? attention_pp_kernel<0u, 3>
               : poly == 0x3333 ? attention_pp_kernel<0x3333u>
               : poly == 0x7777 ? attention_pp_kernel<0x7777u>
               : poly == 0xFFFF ? attention_pp_kernel<0xFFFFu>
