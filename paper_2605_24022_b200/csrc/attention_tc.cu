@@ -909,13 +909,14 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
           mbar_wait(bar_full(s), par_of(i));
           tc_fence_after();
         }
-        const uint32_t k_tile = sKV + s * TILE_BYTES;
-        const uint32_t q_tile = sQ + x * TILE_BYTES;
+        // descriptors are linear in the (16-B unit) start address: build the
+        // tile's once and step them by the K-slice offset
+        const uint64_t qd = sdesc(sQ + x * TILE_BYTES, 16, 1024);
+        const uint64_t kd = sdesc(sKV + s * TILE_BYTES, 16, 1024);
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * ATOM_BYTES + (kk & 3) * 32;
-          tc_mma(tS(x), sdesc(q_tile + off, 16, 1024), sdesc(k_tile + off, 16, 1024), IDESC_S,
-                 kk > 0);
+          const uint32_t off16 = ((kk >> 2) * ATOM_BYTES + (kk & 3) * 32) >> 4;
+          tc_mma(tS(x), qd + off16, kd + off16, IDESC_S, kk > 0);
         }
         if (x == 1) tc_commit(bar_empty(s));
         tc_commit(bar_sfull(x));
@@ -925,10 +926,10 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
         mbar_wait(bar_pfull(x), (uint32_t)(j & 1));
         if (x == 0) mbar_wait(bar_full(s), par_of(i));
         tc_fence_after();
-        const uint32_t v_tile = sKV + s * TILE_BYTES;
+        const uint64_t vd = sdesc(sKV + s * TILE_BYTES, ATOM_BYTES, 1024);
 #pragma unroll
         for (int kk = 0; kk < BLK_N / 16; ++kk)
-          tc_mma_ts(tO(x), tS(x) + kk * 8, sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024), IDESC_O,
+          tc_mma_ts(tO(x), tS(x) + kk * 8, vd + (uint64_t)(kk * 2048 / 16), IDESC_O,
                     (j > 0 || kk > 0) ? 1u : 0u);
         if (x == 1) tc_commit(bar_empty(s));
         tc_commit(bar_pvdone(x));
