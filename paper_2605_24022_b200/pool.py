@@ -19,14 +19,17 @@ Byte accounting matches the reference: bytes moved per (chunk, layer) =
 
 from __future__ import annotations
 
+import os
 import threading
+import time
 from dataclasses import dataclass
+from pathlib import Path
 
 import numpy as np
 import torch
 
 from . import _dev, _lib
-from .errors import InvalidParam, InvalidPlan, NotFound
+from .errors import InvalidParam, InvalidPlan, IoError, NotFound
 from .spectral import ImportanceRanking, selection_count
 
 
@@ -125,6 +128,24 @@ class KvPool:
         return SparseFetchPlan(self.chunk_ids[c], layer, keep, ranges, n_keep * self.row_bytes * 2,
                                n_keep)
 
+    # -- tier model / profiling (ct/cachepool.py:483-529) -----------------------
+    def modeled_fetch_time(self, plan: SparseFetchPlan, tier=None) -> float:
+        """Modelled read time of a plan on `tier` (default: the cpu-mem preset
+        for a pinned pool, gpu-sim for an HBM pool)."""
+        from .pipesim import TIER_PRESETS
+        tier = tier or TIER_PRESETS["cpu-mem" if self.location == "pinned" else "gpu-sim"]
+        return tier.read_time(plan.expected_bytes)
+
+    def measure_transfer_cost(self, tier, sample_bytes: int,
+                              bytes_per_token: int | None = None) -> float:
+        """t_i for `tier` exactly as the reference computes it (scheduler.calibrate
+        calls this when no profile is injected); bytes_per_token defaults to a
+        K+V row of this pool.  The B200 PCIe rate itself is measured by
+        scheduler.measure_h2d_per_token."""
+        if bytes_per_token is None:
+            bytes_per_token = self.row_bytes * 2
+        return transfer_cost_per_token(tier, sample_bytes, bytes_per_token)
+
     def fetch_sparse(self, plan: SparseFetchPlan, stream=None):
         """Move exactly the planned bytes to HBM; return (K [keep,H,D], V, keep)
         in ascending token order like the reference."""
@@ -157,6 +178,39 @@ class KvPool:
         _lib.call("ct_gather_rows", _dev.ptr(stage), _dev.ptr(rows), n_keep, 2 * self.row_bytes,
                   _dev.ptr(kv), _dev.stream_handle(stream))
         return kv[:, 0], kv[:, 1], plan.keep_indices
+
+
+def transfer_cost_per_token(tier, sample_bytes: int, bytes_per_token: int) -> float:
+    """Per-token transfer cost t_i of a tier (ct/cachepool.py:489-529): the
+    analytic model for simulated tiers, a timed sequential read of
+    sample_bytes for file-backed ones (tier.backing = directory)."""
+    if sample_bytes <= 0:
+        raise InvalidParam("sample_bytes must be > 0")
+    tokens = sample_bytes / bytes_per_token
+    if tier.backing is None:
+        return tier.read_time(sample_bytes) / tokens
+    try:
+        root = Path(tier.backing)
+        root.mkdir(parents=True, exist_ok=True)
+        probe = root / ".transfer_probe"
+        payload = os.urandom(min(sample_bytes, 1 << 20))
+        with open(probe, "wb") as f:
+            written = 0
+            while written < sample_bytes:
+                piece = payload[: sample_bytes - written]
+                f.write(piece)
+                written += len(piece)
+            f.flush()
+            os.fsync(f.fileno())
+        start = time.perf_counter()
+        with open(probe, "rb") as f:
+            while f.read(1 << 20):
+                pass
+        elapsed = time.perf_counter() - start
+        probe.unlink(missing_ok=True)
+    except OSError as e:
+        raise IoError(f"transfer probe failed on {tier.backing}: {e}") from e
+    return max(elapsed, 1e-12) / tokens
 
 
 def ctypes_ptr_array(vals):

@@ -109,3 +109,21 @@ def test_timeline_csv_round_trip():
     csv = P.timeline_to_csv(tl)
     assert csv.splitlines()[0] == "stream,layer,start_s,end_s,label"
     assert len(csv.splitlines()) == 1 + 3 * 4
+
+
+def test_transfer_cost_matches_reference_model(tmp_path):
+    """Pool transfer profiling (ct/cachepool.py:489-529): analytic tiers give
+    read_time / tokens exactly; a file-backed tier times a real read (> 0)."""
+    from paper_2605_24022_b200.errors import InvalidParam
+    from paper_2605_24022_b200.pipesim import TIER_PRESETS, TierConfig
+    from paper_2605_24022_b200.pool import transfer_cost_per_token
+    bpt = 8 * 128 * 4 * 2
+    for name, tier in TIER_PRESETS.items():
+        got = transfer_cost_per_token(tier, 1 << 20, bpt)
+        assert got == tier.read_time(1 << 20) / ((1 << 20) / bpt), name
+    disk = TierConfig("ssd", read_bw=535e6, write_bw=445e6, backing=str(tmp_path))
+    assert transfer_cost_per_token(disk, 1 << 18, bpt) > 0
+    assert not (tmp_path / ".transfer_probe").exists()
+    import pytest
+    with pytest.raises(InvalidParam):
+        transfer_cost_per_token(disk, 0, bpt)
