@@ -149,6 +149,16 @@ def _mm_f32(a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     return torch.mm(a, w, out_dtype=torch.float32)
 
 
+def _residual_mm(h: torch.Tensor, a: torch.Tensor, w: torch.Tensor) -> None:
+    """h += a @ w in the GEMM epilogue (cuBLAS beta = 1, f32 C/D, bf16 or f32
+    A/B): the residual add of ct/toymodel.py:184,189 without a separate f32
+    delta round trip through HBM."""
+    if a.dtype == torch.float32:
+        h.addmm_(a, w)
+    else:
+        torch.ops.aten.addmm.dtype_out(h, a, w, torch.float32, beta=1, alpha=1, out=h)
+
+
 def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n_ctx: int,
                caches: Sequence, reuse: Callable[[int], None] | None = None,
                record_attention: bool = False, logits_rows: str | None = "all",
@@ -219,8 +229,8 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
                 _dev.ptr(scratch), dtc, _dev.ptr(part), _dev.ptr(_dev.workspace(wsr, "record")),
                 wsr, st), "ct_selective_attention")
             probs_all.append(part)
-        o = _mm_f32(buf.ctx, w["wo"])
-        _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), _dev.ptr(o), _lib.CT_F32, a, hid,
+        _residual_mm(buf.h, buf.ctx, w["wo"])
+        _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), None, _lib.CT_F32, a, hid,
                   NORM_EPS, _dev.ptr(buf.x), dtc, st)
         kind = cfg.mlp_kind
         if kind:
@@ -230,8 +240,8 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
             inter = buf.act.shape[1]
             _lib.call("ct_mlp_act", _dev.ptr(buf.gu), a, inter, dtc, 1 if kind == "relu" else 0,
                       _dev.ptr(buf.act), dtc, st)
-            dlt = _mm_f32(buf.act, down)
-            _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), _dev.ptr(dlt), _lib.CT_F32, a,
+            _residual_mm(buf.h, buf.act, down)
+            _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), None, _lib.CT_F32, a,
                       hid, NORM_EPS, _dev.ptr(buf.x), dtc, st)
         if hook is not None:
             hook(l, "end")
