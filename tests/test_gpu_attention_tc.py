@@ -104,3 +104,25 @@ def test_tc_attention_f32_output_and_large_scores():
     want = _ref(q, pos, k, v, hq, hkv)
     err = (out - want).abs().max().item() / want.abs().max().item()
     assert err < 1e-2, err
+
+
+def test_tc_attention_randomised_geometries_deterministic():
+    """tools/attn_fuzz.py at a CI-sized case count: random GQA group (1-16),
+    kv heads, query count, context, sorted/unsorted positions, score scale and a
+    key-scale ramp (running-max growth -> lazy O rescale), each launched twice
+    (bit-identical) and checked on sampled rows against PyTorch fp32."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    import importlib.util
+    from pathlib import Path
+    path = Path(__file__).resolve().parents[1] / "tools" / "attn_fuzz.py"
+    spec = importlib.util.spec_from_file_location("attn_fuzz", path)
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    import sys
+    argv = sys.argv
+    try:
+        sys.argv = ["attn_fuzz", "12", "7"]
+        mod.main()
+    finally:
+        sys.argv = argv
