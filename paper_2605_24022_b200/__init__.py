@@ -29,6 +29,10 @@ _LAZY = {
     "STRATEGIES": "experiments", "strategy_ranking": "experiments",
     "effective_ratio": "experiments", "run_selection_experiment": "experiments",
     "FrequencyTokenRanker": "estimators", "RatioCalibrator": "estimators",
+    # serving surface: resident pool + preallocated per-request engine
+    "KvPool": "pool", "SelectivePrefillEngine": "pipeline", "FullPrefillEngine": "pipeline",
+    "prepare_pool": "offline", "calibrate": "scheduler", "SearchConfig": "scheduler",
+    "HardwareProfile": "scheduler",
 }
 
 
