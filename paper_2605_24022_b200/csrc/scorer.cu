@@ -629,6 +629,208 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
   for (int n = threadIdx.x; n < N; n += THREADS) out[n] = acc[n] * inv_n2;
 }
 
+// ---------------------------------------------------------------------------
+// Mixed-radix path for smooth lengths N = 2^a 3^b 5^c 7^d (e.g. 96, 1000, 1536,
+// 3000) that are not powers of two: the same forward FFT -> band mask ->
+// inverse FFT -> |recon|^2 as above, Stockham passes of radix 8/4/2/3/5/7
+// chosen at run time, ping-pong shared-memory buffers (one barrier per pass).
+// N with a prime factor > 7 keeps the direct circulant path.
+// ---------------------------------------------------------------------------
+constexpr int MR_THREADS = 512;
+constexpr int MR_MAX_N = 5120;  // f64: 2 x 5120 x 16 B buffers + 40 KB energies
+constexpr int MR_MAX_PASSES = 16;
+
+struct MrPlan {
+  int n_pass;
+  int radix[MR_MAX_PASSES];
+};
+
+// W_R^m = (cos 2 pi m / R, sin 2 pi m / R), correctly rounded, m = 0..R-1
+__constant__ double c_cos3[3] = {1.0, -0.5, -0.5};
+__constant__ double c_sin3[3] = {0.0, 0.8660254037844386, -0.8660254037844386};
+__constant__ double c_cos5[5] = {1.0, 0.30901699437494745, -0.8090169943749475, -0.8090169943749475,
+                                 0.30901699437494745};
+__constant__ double c_sin5[5] = {0.0, 0.9510565162951535, 0.5877852522924731, -0.5877852522924731,
+                                 -0.9510565162951535};
+__constant__ double c_cos7[7] = {1.0, 0.6234898018587335, -0.2225209339563144, -0.9009688679024191,
+                                 -0.9009688679024191, -0.2225209339563144, 0.6234898018587335};
+__constant__ double c_sin7[7] = {0.0, 0.7818314824680298, 0.9749279121818236, 0.4338837391175581,
+                                 -0.4338837391175581, -0.9749279121818236, -0.7818314824680298};
+
+// y[k] = sum_n x[n] W_R^{-+nk} for a small prime R (forward sign -, inverse +)
+template <int R, bool INV, typename T>
+__device__ __forceinline__ void dft_prime(cpx<T>* v) {
+  const double* cs = R == 3 ? c_cos3 : R == 5 ? c_cos5 : c_cos7;
+  const double* sn = R == 3 ? c_sin3 : R == 5 ? c_sin5 : c_sin7;
+  cpx<T> y[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    cpx<T> acc = v[0];
+#pragma unroll
+    for (int n = 1; n < R; ++n) {
+      const int m = (n * k) % R;
+      const T c = (T)cs[m], sv = INV ? (T)sn[m] : (T)-sn[m];
+      acc.x += v[n].x * c - v[n].y * sv;
+      acc.y += v[n].x * sv + v[n].y * c;
+    }
+    y[k] = acc;
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = y[k];
+}
+
+template <int R, bool INV, typename T>
+__device__ __forceinline__ void dft_any(cpx<T>* v) {
+  if constexpr (R == 2 || R == 4 || R == 8) dft_small<R, INV>(v);
+  else dft_prime<R, INV>(v);
+}
+
+// One Stockham pass (radix R, Ns = product of the earlier radices) from `in`
+// to `out` over S signals.  MASK zeroes the band-rejected bins on load (first
+// inverse pass); ENERGY stores |z|^2 in .x (last inverse pass).
+template <int R, bool INV, typename T>
+__device__ __forceinline__ void mr_pass(const cpx<T>* in, cpx<T>* out, int S, int N, int Ns,
+                                        const cpx<T>* __restrict__ tw, bool mask, int cutoff,
+                                        bool energy) {
+  const int NB = N / R;
+  const int step = N / (Ns * R);
+  for (int b = threadIdx.x; b < S * NB; b += MR_THREADS) {
+    const int sg = b / NB, j = b - sg * NB;
+    const int jm = j % Ns;
+    cpx<T> v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int idx = j + r * NB;
+      cpx<T> val = in[sg * N + idx];
+      if (mask) {
+        const int kk = idx < N - idx ? idx : N - idx;
+        if (cutoff >= 0 ? kk >= cutoff : kk < -cutoff - 1) val = {(T)0, (T)0};
+      }
+      if (r > 0 && jm > 0) {
+        // jm * step * r < (N / R) * R = N: no modular reduction needed
+        cpx<T> w = tw[jm * step * r];
+        if (INV) w.y = -w.y;
+        val = cmul(val, w);
+      }
+      v[r] = val;
+    }
+    dft_any<R, INV>(v);
+    const int base = (j / Ns) * Ns * R + jm;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (energy) out[sg * N + base + r * Ns] = {v[r].x * v[r].x + v[r].y * v[r].y, (T)0};
+      else out[sg * N + base + r * Ns] = v[r];
+    }
+  }
+}
+
+template <bool INV, typename T>
+__device__ __forceinline__ void mr_pass_any(int R, const cpx<T>* in, cpx<T>* out, int S, int N,
+                                            int Ns, const cpx<T>* tw, bool mask, int cutoff,
+                                            bool energy) {
+  switch (R) {
+    case 8: mr_pass<8, INV>(in, out, S, N, Ns, tw, mask, cutoff, energy); break;
+    case 4: mr_pass<4, INV>(in, out, S, N, Ns, tw, mask, cutoff, energy); break;
+    case 2: mr_pass<2, INV>(in, out, S, N, Ns, tw, mask, cutoff, energy); break;
+    case 3: mr_pass<3, INV>(in, out, S, N, Ns, tw, mask, cutoff, energy); break;
+    case 5: mr_pass<5, INV>(in, out, S, N, Ns, tw, mask, cutoff, energy); break;
+    default: mr_pass<7, INV>(in, out, S, N, Ns, tw, mask, cutoff, energy); break;
+  }
+}
+
+// grid: x = lane block, y = tensor, z = c*L + l; S = max(1, 4096 / N) signals
+// (2S lanes) in flight per CTA.
+template <typename T, typename IN>
+__global__ void __launch_bounds__(MR_THREADS, 1)
+fftmr_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int N, int L,
+                    int lanes, int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff,
+                    const cpx<T>* __restrict__ tw, MrPlan plan, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int S = N >= 4096 ? 1 : 4096 / N;
+  cpx<T>* buf0 = reinterpret_cast<cpx<T>*>(smem_raw);
+  cpx<T>* buf1 = buf0 + S * N;
+  double* acc = reinterpret_cast<double*>(buf1 + S * N);
+  const int lb = blockIdx.x, tensor = blockIdx.y;
+  const int c = blockIdx.z / L, l = blockIdx.z % L;
+  const IN* base = (tensor == 0 ? keys : values) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer;
+  const int lane0 = lb * LANE_BLOCK, lane_end = min(lanes, lane0 + LANE_BLOCK);
+  for (int n = threadIdx.x; n < N; n += MR_THREADS) acc[n] = 0.0;
+  for (int g0 = lane0; g0 < lane_end; g0 += 2 * S) {
+    for (int q = threadIdx.x; q < S * N; q += MR_THREADS) {
+      const int sg = q / N, n = q - sg * N;
+      const int la = g0 + 2 * sg, lbn = la + 1;
+      const IN* row = base + (int64_t)n * ld_token;
+      buf0[q] = {la < lane_end ? (T)load_as_double(row + la) : (T)0,
+                 lbn < lane_end ? (T)load_as_double(row + lbn) : (T)0};
+    }
+    __syncthreads();
+    cpx<T>* src = buf0;
+    cpx<T>* dst = buf1;
+    int Ns = 1;
+    for (int p = 0; p < plan.n_pass; ++p) {  // forward
+      mr_pass_any<false>(plan.radix[p], src, dst, S, N, Ns, tw, false, cutoff, false);
+      Ns *= plan.radix[p];
+      __syncthreads();
+      cpx<T>* t = src; src = dst; dst = t;
+    }
+    Ns = 1;
+    for (int p = 0; p < plan.n_pass; ++p) {  // inverse, mask on the first pass
+      mr_pass_any<true>(plan.radix[p], src, dst, S, N, Ns, tw, p == 0, cutoff,
+                        p == plan.n_pass - 1);
+      Ns *= plan.radix[p];
+      __syncthreads();
+      cpx<T>* t = src; src = dst; dst = t;
+    }
+    // energies in src[sg][n].x: fixed-order sum over the group's signals
+    for (int n = threadIdx.x; n < N; n += MR_THREADS) {
+      double e = 0.0;
+      for (int sg = 0; sg < S; ++sg) e += (double)src[sg * N + n].x;
+      acc[n] += e;
+    }
+    __syncthreads();
+  }
+  const double inv_n2 = 1.0 / ((double)N * (double)N);
+  const int nlb = gridDim.x;
+  double* out = partial + ((((int64_t)blockIdx.z * 2 + tensor) * nlb) + lb) * N;
+  for (int n = threadIdx.x; n < N; n += MR_THREADS) out[n] = acc[n] * inv_n2;
+}
+
+static bool mr_plan(int64_t N, MrPlan* plan) {
+  if (N < 2 || N > MR_MAX_N) return false;
+  int64_t m = N;
+  plan->n_pass = 0;
+  const int order[6] = {8, 4, 2, 3, 5, 7};
+  for (int i = 0; i < 6; ++i) {
+    const int r = order[i];
+    while (m % r == 0) {
+      if (plan->n_pass == MR_MAX_PASSES) return false;
+      plan->radix[plan->n_pass++] = r;
+      m /= r;
+    }
+  }
+  return m == 1;
+}
+
+template <typename T>
+static size_t mr_smem(int64_t N) {
+  const int64_t S = N >= 4096 ? 1 : 4096 / N;
+  return (size_t)(2 * S * N) * sizeof(cpx<T>) + (size_t)N * sizeof(double);
+}
+
+template <typename T, typename IN>
+static int launch_mr(const void* k, const void* v, int64_t N, int L, int C, int lanes, int64_t ldt,
+                     int64_t ldl, int64_t ldc, int cutoff, const void* tw, const MrPlan& plan,
+                     double* partial, cudaStream_t st) {
+  auto kern = fftmr_energy_kernel<T, IN>;
+  const size_t smem = mr_smem<T>(N);
+  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
+  dim3 grid(nlb, 2, C * L);
+  kern<<<grid, MR_THREADS, smem, st>>>((const IN*)k, (const IN*)v, (int)N, L, lanes, ldt, ldl, ldc,
+                                       cutoff, (const cpx<T>*)tw, plan, partial);
+  return check_launch("fftmr_energy_kernel");
+}
+
 // Circulant band kernel p[m] = (1/N) sum_{k in band} w_k cos(2 pi k m/N) over
 // rfft bins k in [0, N/2] (w_k = 1 for DC and an even-N Nyquist bin, else 2):
 // the exact impulse response of rfft -> zero the other bins -> irfft.  Low band
@@ -1000,6 +1202,25 @@ extern "C" int ct_score_chunks_band(const void* keys, const void* values, int dt
                                                   ld_token, ld_layer, ld_chunk, cut, tw_f,
                                                   partial, st);
     }
+    if (rc) return rc;
+  } else if (MrPlan plan; mr_plan(N, &plan)) {
+    twiddle_table<<<(unsigned)((N + 255) / 256), 256, 0, st>>>((int)N, (cpx<double>*)tw_d,
+                                                                (cpx<float>*)tw_f);
+    if ((rc = check_launch("twiddle_table"))) return rc;
+    if (precision == CT_F64)
+      rc = dtype == CT_F32
+               ? launch_mr<double, float>(keys, values, N, (int)L, (int)C, (int)lanes, ld_token,
+                                          ld_layer, ld_chunk, cut, tw_d, plan, partial, st)
+               : launch_mr<double, __nv_bfloat16>(keys, values, N, (int)L, (int)C, (int)lanes,
+                                                  ld_token, ld_layer, ld_chunk, cut, tw_d, plan,
+                                                  partial, st);
+    else
+      rc = dtype == CT_F32
+               ? launch_mr<float, float>(keys, values, N, (int)L, (int)C, (int)lanes, ld_token,
+                                         ld_layer, ld_chunk, cut, tw_f, plan, partial, st)
+               : launch_mr<float, __nv_bfloat16>(keys, values, N, (int)L, (int)C, (int)lanes,
+                                                 ld_token, ld_layer, ld_chunk, cut, tw_f, plan,
+                                                 partial, st);
     if (rc) return rc;
   } else {
     double* p = (double*)tw_d;

@@ -119,12 +119,14 @@ def test_big_chunks_config2_geometry(ct, precision):
         assert np.array_equal(outb["agg_order"][0].cpu().numpy(), g[f"s{s}_bf16_agg"])
 
 
-@pytest.mark.parametrize("n", [512, 1024, 2048, 4096])
+@pytest.mark.parametrize("n", [512, 1024, 2048, 4096,            # register-resident path
+                               2, 6, 96, 1000, 1536, 3000, 5120])  # mixed radix 2/3/5/7
 @pytest.mark.parametrize("lanes", [(2, 8), (13, 10)])
 @pytest.mark.parametrize("alpha", [0.5, 0.13, 1.0])
 def test_scorer_fft_lengths_vs_oracle(ct, n, lanes, alpha):
-    """Register-resident Stockham path (N = 512..4096) incl. ragged lane counts
-    (lanes not a multiple of the tile width / 128-lane block) vs the oracle."""
+    """Register-resident Stockham path (N = 512..4096) and the mixed-radix path
+    (smooth N), incl. ragged lane counts (lanes not a multiple of the tile width /
+    128-lane block) vs the oracle."""
     from paper_2605_24022_b200.spectral import score_device
     h, d = lanes
     rng = np.random.default_rng(n + h + int(alpha * 100))

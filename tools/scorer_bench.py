@@ -13,9 +13,10 @@ from paper_2605_24022_b200.spectral import score_device  # noqa: E402
 
 def main():
     C = int(sys.argv[1]) if len(sys.argv) > 1 else 16
+    N = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
     gen = torch.Generator(device="cuda").manual_seed(0)
-    k = torch.randn((C, 32, 2048, 8, 128), device="cuda", generator=gen).to(torch.bfloat16)
-    v = torch.randn((C, 32, 2048, 8, 128), device="cuda", generator=gen).to(torch.bfloat16)
+    k = torch.randn((C, 32, N, 8, 128), device="cuda", generator=gen).to(torch.bfloat16)
+    v = torch.randn((C, 32, N, 8, 128), device="cuda", generator=gen).to(torch.bfloat16)
     nbytes = 2 * k.numel() * 2
     for prec in ("f64", "f32"):
         score_device(k, v, 0.5, prec, want_layer_order=False)
@@ -28,7 +29,7 @@ def main():
         torch.cuda.synchronize()
         ms = s.elapsed_time(e) / 3
         print(f"scorer {prec}: {C} chunks {ms:.2f} ms  {nbytes / ms / 1e6:.0f} GB/s  "
-              f"({ms / C:.3f} ms per 2048-token chunk of 32 layers)")
+              f"({ms / C:.3f} ms per {N}-token chunk of 32 layers)")
 
 
 if __name__ == "__main__":
