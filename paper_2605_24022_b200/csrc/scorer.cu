@@ -738,15 +738,15 @@ __device__ __forceinline__ void mr_pass_any(int R, const cpx<T>* in, cpx<T>* out
   }
 }
 
-// grid: x = lane block, y = tensor, z = c*L + l; S = max(1, 4096 / N) signals
-// (2S lanes) in flight per CTA.
+// grid: x = lane block, y = tensor, z = c*L + l; S signals (2S lanes) in
+// flight per CTA, as many as the ping-pong buffers leave room for.
 template <typename T, typename IN>
 __global__ void __launch_bounds__(MR_THREADS, 1)
 fftmr_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int N, int L,
                     int lanes, int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff,
-                    const cpx<T>* __restrict__ tw, MrPlan plan, double* __restrict__ partial) {
+                    const cpx<T>* __restrict__ tw, MrPlan plan, int S,
+                    double* __restrict__ partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int S = N >= 4096 ? 1 : 4096 / N;
   cpx<T>* buf0 = reinterpret_cast<cpx<T>*>(smem_raw);
   cpx<T>* buf1 = buf0 + S * N;
   double* acc = reinterpret_cast<double*>(buf1 + S * N);
@@ -812,9 +812,16 @@ static bool mr_plan(int64_t N, MrPlan* plan) {
 }
 
 template <typename T>
+static int mr_signals(int64_t N) {
+  const int64_t room = 227 * 1024 - N * (int64_t)sizeof(double);
+  int64_t S = room / (2 * N * (int64_t)sizeof(cpx<T>));
+  if (S > 64) S = 64;  // 128-lane blocks
+  return (int)(S < 1 ? 1 : S);
+}
+
+template <typename T>
 static size_t mr_smem(int64_t N) {
-  const int64_t S = N >= 4096 ? 1 : 4096 / N;
-  return (size_t)(2 * S * N) * sizeof(cpx<T>) + (size_t)N * sizeof(double);
+  return (size_t)(2 * mr_signals<T>(N) * N) * sizeof(cpx<T>) + (size_t)N * sizeof(double);
 }
 
 template <typename T, typename IN>
@@ -827,7 +834,7 @@ static int launch_mr(const void* k, const void* v, int64_t N, int L, int C, int 
   const int nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
   dim3 grid(nlb, 2, C * L);
   kern<<<grid, MR_THREADS, smem, st>>>((const IN*)k, (const IN*)v, (int)N, L, lanes, ldt, ldl, ldc,
-                                       cutoff, (const cpx<T>*)tw, plan, partial);
+                                       cutoff, (const cpx<T>*)tw, plan, mr_signals<T>(N), partial);
   return check_launch("fftmr_energy_kernel");
 }
 
