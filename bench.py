@@ -405,15 +405,23 @@ def run_ours(args, rank, world, local_rank):
     fp64_peak = 64 * 2 * 148 * 1.965e9 / 1e12
     value = world * args.steps / (total_ms * 1e-3)
     e2e_val = world * args.steps / (e2e_total * 1e-3)
-    lin_flops = 2.0 * eng.A * sum(w.numel() for layer in model.layers for w in layer.values())
-    lin_flops += 2.0 * cfg.hidden_dim * cfg.vocab_size
-    step_flops = lin_flops + att_flops * L
+    # FLOPs actually performed per request: every layer projects q|k|v for all
+    # A rows (the last layer's K/V complete the blended cache), but the last
+    # layer's attention / O-projection / MLP run on the final row only -- the
+    # first-token logits read nothing else (prefill.run_layers, prune_last);
+    # the full-recompute baseline is pruned the same way.
+    def request_flops(rows, att_per_layer, last_pos):
+        qkv_w = sum(layer["wqkv"].numel() for layer in model.layers)
+        rest_w = sum(w.numel() for layer in model.layers for k, w in layer.items() if k != "wqkv")
+        rest_last = sum(w.numel() for k, w in model.layers[-1].items() if k != "wqkv")
+        return (2.0 * rows * qkv_w + 2.0 * rows * (rest_w - rest_last) + 2.0 * rest_last
+                + 2.0 * cfg.hidden_dim * cfg.vocab_size + att_per_layer * (L - 1)
+                + 4.0 * cfg.n_heads * cfg.head_dim * (last_pos + 1))
+    step_flops = request_flops(eng.A, att_flops, eng.n_ctx - 1)
     full_flops = None
     if full_ms is not None:
         n = eng.n_ctx
-        full_flops = (2.0 * n * sum(w.numel() for layer in model.layers for w in layer.values())
-                      + 2.0 * cfg.hidden_dim * cfg.vocab_size
-                      + 4.0 * cfg.n_heads * cfg.head_dim * n * (n + 1) / 2 * L)
+        full_flops = request_flops(n, 4.0 * cfg.n_heads * cfg.head_dim * n * (n + 1) / 2, n - 1)
 
     cpu = None
     if world == 1 and not args.no_cpu:

@@ -796,30 +796,47 @@ attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
 // of one overlaps the TMEM load / row max / P store of the other.  K/V bytes
 // per FLOP from L2 halve versus the single-tile kernel.
 // ---------------------------------------------------------------------------
+template <int SLOTS_ = 5>
 struct SmemPP {
-  static constexpr int SLOTS = 5;
+  static constexpr int SLOTS = SLOTS_;
   static constexpr int Q = 0;                        // two Q tiles
   static constexpr int KV = Q + 2 * TILE_BYTES;
   static constexpr int BAR = KV + SLOTS * TILE_BYTES;
-  // q, full[4], empty[4], per tile: sfull, pfull, pvdone
+  // q, full[SLOTS], empty[SLOTS], per tile: sfull, pfull, pvdone
   static constexpr int NBAR = 1 + 2 * SLOTS + 6;
-  static constexpr int TMEM_PTR = BAR + NBAR * 8;
+  // split-row variant: [2 parity][2 tiles][2 halves][128 rows] f32 max / sum exchange
+  static constexpr int XCH = BAR + NBAR * 8;
+  static constexpr int XCH_BYTES = SLOTS_ < 5 ? 2 * 2 * 2 * 128 * 4 : 0;
+  static constexpr int TMEM_PTR = XCH + XCH_BYTES;
   static constexpr int TOTAL = TMEM_PTR + 16;
 };
 
-template <uint32_t POLY_MASK, int SCHED = 1>
-__global__ void __launch_bounds__(32 * 10, 1)
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// SPLIT = 2: two softmax threads per tile row (16 softmax warps; warp
+// x*8 + h*4 + q owns TMEM lane quarter q of tile x and key columns
+// [64h, 64h+64) of every block), halving the per-tile S -> softmax -> PV
+// latency; the two halves agree on the running max through a 64-thread named
+// barrier per lane quarter, P of half h lands in TMEM columns [64h, 64h+32) of
+// S, and each half rescales / stores its 64 O columns.  Needs the exchange
+// area, so it runs with 4 K/V slots.
+template <uint32_t POLY_MASK, int SCHED = 1, int SPLIT = 1, int SLOTS = 5>
+__global__ void __launch_bounds__(32 * (8 * SPLIT + 2), 1)
 attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const Params p) {
-  constexpr int TMA_WARP = 8, MMA_WARP = 9;
-  constexpr int NSLOT = SmemPP::SLOTS;
+  using SM = SmemPP<SLOTS>;
+  constexpr int TMA_WARP = 8 * SPLIT, MMA_WARP = 8 * SPLIT + 1;
+  constexpr int NSLOT = SM::SLOTS;
+  static_assert(SPLIT == 1 || (SPLIT == 2 && SM::XCH_BYTES > 0), "split rows need the exchange area");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sQ = base + SmemPP::Q, sKV = base + SmemPP::KV;
-  const uint32_t bar0 = base + SmemPP::BAR;
+  const uint32_t sQ = base + SM::Q, sKV = base + SM::KV;
+  const uint32_t bar0 = base + SM::BAR;
   const uint32_t bar_q = bar0;
   auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };
   auto bar_empty = [&](int s) { return bar0 + (1 + NSLOT + s) * 8; };
@@ -827,7 +844,8 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
   auto bar_sfull = [&](int x) { return bar0 + (B2 + x) * 8; };
   auto bar_pfull = [&](int x) { return bar0 + (B2 + 2 + x) * 8; };
   auto bar_pvdone = [&](int x) { return bar0 + (B2 + 4 + x) * 8; };
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + SmemPP::TMEM_PTR);
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + SM::TMEM_PTR);
+  float* xch = reinterpret_cast<float*>(gbase + SM::XCH);  // [parity][tile][half][row]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // longest units first; unit = two adjacent query blocks of kv head g
@@ -850,7 +868,7 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(bar_sfull(x), 1);
-      mbar_init(bar_pfull(x), 4);  // one elected arrive per softmax warp of the tile
+      mbar_init(bar_pfull(x), 4 * SPLIT);  // one elected arrive per softmax warp of the tile
       mbar_init(bar_pvdone(x), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -928,9 +946,13 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
         tc_fence_after();
         const uint64_t vd = sdesc(sKV + s * TILE_BYTES, ATOM_BYTES, 1024);
 #pragma unroll
-        for (int kk = 0; kk < BLK_N / 16; ++kk)
-          tc_mma_ts(tO(x), tS(x) + kk * 8, vd + (uint64_t)(kk * 2048 / 16), IDESC_O,
+        for (int kk = 0; kk < BLK_N / 16; ++kk) {
+          // P of keys [16kk, 16kk+16): bf16x2 columns 8kk (one softmax thread
+          // per row) or 64*(kk/4) + 8*(kk%4) (half h stores over its own S columns)
+          const uint32_t pcol = SPLIT == 1 ? kk * 8 : (kk >> 2) * 64 + (kk & 3) * 8;
+          tc_mma_ts(tO(x), tS(x) + pcol, vd + (uint64_t)(kk * 2048 / 16), IDESC_O,
                     (j > 0 || kk > 0) ? 1u : 0u);
+        }
         if (x == 1) tc_commit(bar_empty(s));
         tc_commit(bar_pvdone(x));
       };
@@ -947,38 +969,51 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
     }
   } else {
     // ------------------------------------------------------------ softmax
-    const int x = warp >> 2;                  // tile
+    constexpr int KEYS = BLK_N / SPLIT;       // key columns per softmax thread
+    const int x = warp / (4 * SPLIT);         // tile
+    const int hh = SPLIT == 1 ? 0 : (warp >> 2) & 1;  // key-column half
+    const int col0 = hh * KEYS;
     const int m = (warp & 3) * 32 + lane;     // TMEM lane / tile row
+    const int xbar = 1 + x * 4 + (warp & 3);  // named barrier of the row's two halves
     const int qi = m / p.G, hj = m % p.G;
     const int a = (qb0 + x) * p.QB + qi;
     const bool valid = a < p.A;
     const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
     float m_used = -INFINITY, l = 0.f;
-    uint32_t r[BLK_N];
+    uint32_t r[KEYS];
     for (int j = 0; j < nb; ++j) {
       mbar_wait(bar_sfull(x), (uint32_t)(j & 1));
       __syncwarp();
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < BLK_N / 32; ++c) tmem_ld32(tS(x) + lane_off + c * 32, r + c * 32);
+      for (int c = 0; c < KEYS / 32; ++c) tmem_ld32(tS(x) + lane_off + col0 + c * 32, r + c * 32);
 #pragma unroll
-      for (int c = 0; c < BLK_N / 32; ++c) tmem_wait_ld32(r + c * 32);
-      const int kbase = j * BLK_N;
-      const bool need_mask = kbase + BLK_N - 1 > pos;
+      for (int c = 0; c < KEYS / 32; ++c) tmem_wait_ld32(r + c * 32);
+      const int kbase = j * BLK_N + col0;
+      const bool need_mask = kbase + KEYS - 1 > pos;
       if (need_mask) {
 #pragma unroll
-        for (int c = 0; c < BLK_N; ++c)
+        for (int c = 0; c < KEYS; ++c)
           if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
       }
       float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int c = 0; c < BLK_N; c += 8) {
+      for (int c = 0; c < KEYS; c += 8) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
           mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
       }
-      const float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
+      float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
+      if constexpr (SPLIT == 2) {
+        // both halves of the row must use the same running max: exchange the
+        // block maxima (double buffered by block parity, so a fast half never
+        // overwrites a value its partner has not read yet)
+        float* xb = xch + (((j & 1) * 2 + x) * 2) * 128;
+        xb[hh * 128 + m] = mx;
+        named_bar_sync(xbar, 64);
+        mx = fmaxf(mx, xb[(hh ^ 1) * 128 + m]);  // symmetric: both halves get the same value
+      }
       const float m_new = fmaxf(m_used, mx);
       const bool grow = m_new > m_used + p.lazy_thresh;
       const bool any_grow = __any_sync(0xffffffffu, grow);
@@ -988,7 +1023,7 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
       const uint64_t nm2 = pk2(-m_used, -m_used);
       uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
       // P_j (bf16x2) -> TMEM columns [0, 64) of S_x, 32 keys per store
-      if constexpr (SCHED == 0) {
+      if constexpr (SCHED == 0 && SPLIT == 1) {
         auto chunk = [&](auto cc) {
           constexpr int c = decltype(cc)::value;
           uint32_t pk[16];
@@ -1007,7 +1042,7 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
         // run back to back (MUFU / polynomial), then packing + row sums + TMEM
         // stores, so one warp keeps the MUFU pipe fed without per-chunk chains
 #pragma unroll
-        for (int hb = 0; hb < 2; ++hb) {
+        for (int hb = 0; hb < KEYS / 64; ++hb) {
           uint32_t* rh = r + hb * 64;
 #pragma unroll
           for (int c = 0; c < 64; c += 2) {
@@ -1026,7 +1061,7 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
           } else {
 #pragma unroll
             for (int c = 0; c < 64; c += 2) {
-              if ((POLY_MASK >> ((hb * 64 + c) / 8)) & 1) {
+              if ((POLY_MASK >> ((col0 + hb * 64 + c) / 8)) & 1) {
                 uint32_t o0, o1;
                 exp2_poly2(pk2(__uint_as_float(rh[c]), __uint_as_float(rh[c + 1])), o0, o1);
                 rh[c] = o0;
@@ -1046,7 +1081,7 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
               acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e0 | ((uint64_t)e1 << 32));
               pk[t] = pack_bf16(__uint_as_float(e0), __uint_as_float(e1));
             }
-            tmem_st16(tS(x) + lane_off + (hb * 2 + c) * 16, pk);
+            tmem_st16(tS(x) + lane_off + col0 + (hb * 2 + c) * 16, pk);
           }
         }
       }
@@ -1063,13 +1098,14 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
         __syncwarp();
         tc_fence_after();
 #pragma unroll 1
-        for (int c = 0; c < HD / 32; ++c) {
+        for (int c = 0; c < HD / 32 / SPLIT; ++c) {
+          const uint32_t oc = hh * (HD / SPLIT) + c * 32;
           uint32_t o[32];
-          tmem_ld32(tO(x) + lane_off + c * 32, o);
+          tmem_ld32(tO(x) + lane_off + oc, o);
           tmem_wait_ld32(o);
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-          tmem_st32(tO(x) + lane_off + c * 32, o);
+          tmem_st32(tO(x) + lane_off + oc, o);
         }
         tmem_wait_st();
       }
@@ -1080,10 +1116,17 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
     mbar_wait(bar_pvdone(x), (uint32_t)((nb - 1) & 1));
     __syncwarp();
     tc_fence_after();
+    if constexpr (SPLIT == 2) {
+      float* xb = xch + (((nb & 1) * 2 + x) * 2) * 128;
+      xb[hh * 128 + m] = l;
+      named_bar_sync(xbar, 64);
+      l = l + xb[(hh ^ 1) * 128 + m];  // commutative: both halves agree
+    }
     const float inv = valid ? 1.f / l : 0.f;
     const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD;
 #pragma unroll 1
-    for (int c = 0; c < HD / 32; ++c) {
+    for (int cc = 0; cc < HD / 32 / SPLIT; ++cc) {
+      const int c = hh * (HD / 32 / SPLIT) + cc;
       uint32_t o[32];
       tmem_ld32(tO(x) + lane_off + c * 32, o);
       tmem_wait_ld32(o);
@@ -1223,10 +1266,13 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
               : poly == 0x5555 ? attention_pp_kernel<0x5555u>
               : poly == 0x1111 ? attention_pp_kernel<0x1111u>
               : poly == 0x2222 ? attention_pp_kernel<0x2222u> : attention_pp_kernel<0u>;
-    const size_t smem_pp = SmemPP::TOTAL + 1024;
+    int split = 1;
+    if (const char* e = getenv("CT_TC_SPLIT")) split = atoi(e) == 2 ? 2 : 1;
+    if (split == 2) kp = poly == 0x4444 ? attention_pp_kernel<0x4444u, 1, 2, 4> : attention_pp_kernel<0u, 1, 2, 4>;
+    const size_t smem_pp = (split == 2 ? SmemPP<4>::TOTAL : SmemPP<5>::TOTAL) + 1024;
     CT_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pp));
     const unsigned grid_pp = (unsigned)(((prm.n_qblocks + 1) / 2) * Hkv);
-    kp<<<grid_pp, 320, smem_pp, st>>>(mq, mk, mv, prm);
+    kp<<<grid_pp, 32 * (8 * split + 2), smem_pp, st>>>(mq, mk, mv, prm);
     return check_launch("attention_pp_kernel");
   }
   if (ctas == 2)

@@ -164,13 +164,15 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
                record_attention: bool = False, logits_rows: str | None = "all",
                k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None,
                timer=None, hook: Callable[[int, str], None] | None = None,
-               record_rows_from: int | None = None):
+               record_rows_from: int | None = None, prune_last: bool = True):
     """Shared forward engine (ct/toymodel.py:135-193) over device inputs.
 
     tokens/positions: int32 [A] device.  caches[l] = (K, V) [n_ctx, Hkv, D]
     (model dtype).  reuse(l) fills the reused rows of layer l before its
     attention.  record_rows_from=i records probabilities of query rows [i, A)
-    only.  Returns (logits f32 [rows, V] or None, probs list)."""
+    only.  prune_last: with logits_rows "last" / None the last layer's
+    attention and MLP run on the last row only / are skipped (the caches are
+    complete either way).  Returns (logits f32 [rows, V] or None, probs list)."""
     cfg = model.config
     dev = model.device
     a = tokens.numel()
@@ -180,6 +182,7 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
     st = _dev.stream_handle()
     lib = _lib.load()
     buf = buffers or LayerBuffers(model, a, dev)
+    n_layers = len(model.layers)
     params = cfg.rope_params
     table = rope_table(params, n_ctx, "f64" if dt == torch.float32 else "f32", dev)
     wsb = lib.ct_attention_workspace_bytes(a, hq, n_ctx, hkv, d, dtc)
@@ -207,15 +210,30 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
             hook(l, "recomputed")
         if reuse is not None:
             reuse(l)
+        # Last layer: once its K/V rows are in the cache nothing downstream
+        # reads the other rows' outputs, so when only the first-token logits
+        # (or nothing) are wanted, attention / O-projection / MLP run on the
+        # last row alone (or are skipped).  Recording keeps every row.
+        r0 = 0
+        if l == n_layers - 1 and prune_last and not record_attention and record_rows_from is None:
+            if logits_rows is None:
+                if hook is not None:
+                    hook(l, "end")
+                break
+            if logits_rows != "all":
+                r0 = a - 1
+        av = a - r0
+        hv, xv, qv, ctxv, posv = buf.h[r0:], buf.x[r0:], buf.q[r0:], buf.ctx[r0:], positions[r0:]
         probs = (torch.empty((hq, a, n_ctx), dtype=torch.float32, device=dev)
                  if record_attention else None)
-        t0 = timer.start("attention") if timer is not None else None
+        tname = "attention" if r0 == 0 else "attention_last_row"
+        t0 = timer.start(tname) if timer is not None else None
         _lib.check(lib.ct_selective_attention(
-            _dev.ptr(buf.q), _dev.ptr(positions), a, hq, _dev.ptr(kc), _dev.ptr(vc), n_ctx, hkv,
-            d, kc.stride(0), scale, dtc, _dev.ptr(buf.ctx), dtc, _dev.ptr(probs), _dev.ptr(ws),
+            _dev.ptr(qv), _dev.ptr(posv), av, hq, _dev.ptr(kc), _dev.ptr(vc), n_ctx, hkv,
+            d, kc.stride(0), scale, dtc, _dev.ptr(ctxv), dtc, _dev.ptr(probs), _dev.ptr(ws),
             wsb, st), "ct_selective_attention")
         if timer is not None:
-            timer.stop("attention", t0)
+            timer.stop(tname, t0)
         if record_attention:
             probs_all.append(probs)
         elif record_rows_from is not None and record_rows_from < a:
@@ -229,20 +247,21 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
                 _dev.ptr(scratch), dtc, _dev.ptr(part), _dev.ptr(_dev.workspace(wsr, "record")),
                 wsr, st), "ct_selective_attention")
             probs_all.append(part)
-        _residual_mm(buf.h, buf.ctx, w["wo"])
-        _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), None, _lib.CT_F32, a, hid,
-                  NORM_EPS, _dev.ptr(buf.x), dtc, st)
+        _residual_mm(hv, ctxv, w["wo"])
+        _lib.call("ct_residual_rmsnorm", _dev.ptr(hv), None, _lib.CT_F32, av, hid,
+                  NORM_EPS, _dev.ptr(xv), dtc, st)
         kind = cfg.mlp_kind
         if kind:
             up = w["w1"] if kind == "relu" else w["wgu"]
             down = w["w2"] if kind == "relu" else w["wd"]
-            torch.mm(buf.x, up, out=buf.gu)
+            guv, actv = buf.gu[r0:], buf.act[r0:]
+            torch.mm(xv, up, out=guv)
             inter = buf.act.shape[1]
-            _lib.call("ct_mlp_act", _dev.ptr(buf.gu), a, inter, dtc, 1 if kind == "relu" else 0,
-                      _dev.ptr(buf.act), dtc, st)
-            _residual_mm(buf.h, buf.act, down)
-            _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), None, _lib.CT_F32, a,
-                      hid, NORM_EPS, _dev.ptr(buf.x), dtc, st)
+            _lib.call("ct_mlp_act", _dev.ptr(guv), av, inter, dtc, 1 if kind == "relu" else 0,
+                      _dev.ptr(actv), dtc, st)
+            _residual_mm(hv, actv, down)
+            _lib.call("ct_residual_rmsnorm", _dev.ptr(hv), None, _lib.CT_F32, av,
+                      hid, NORM_EPS, _dev.ptr(xv), dtc, st)
         if hook is not None:
             hook(l, "end")
     logits = None

@@ -338,6 +338,27 @@ def test_config1_r1_matches_full_and_r0_pure_reuse(ct):
     assert np.array_equal(K0[512:1024], want)
 
 
+@pytest.mark.parametrize("mlp", [False, True])
+def test_last_layer_pruning_keeps_first_token_and_cache(ct, mlp):
+    """logits_rows="last" runs the last layer's attention / MLP on the final row
+    only: first-token logits match the reference within the fp32 tolerance and
+    the blended caches are bit-identical to the unpruned run."""
+    g = golden("toy_cfg1")
+    tag = "cfg1mlp" if mlp else "cfg1"
+    model = O.Model(O.ModelConfig(seed=0, n_layers=2, mlp=mlp))
+    chunks, ranks = _cfg1_inputs(ct, g, tag)
+    full = ct.selective_prefill(model, chunks, ranks, g[f"{tag}_suffix"], 0.15,
+                                record_attention=False)
+    last = ct.selective_prefill(model, chunks, ranks, g[f"{tag}_suffix"], 0.15,
+                                record_attention=False, logits_rows="last")
+    assert last.logits.shape[0] == 1
+    got = last.logits[-1].double().cpu().numpy()
+    assert O.normwise_rel(got, g[f"{tag}_logits"][-1]) < FP32_TOL
+    assert O.normwise_rel(got, full.logits[-1].double().cpu().numpy()) < FP32_TOL
+    for (k1, v1), (k2, v2) in zip(full.kv, last.kv):
+        assert torch.equal(k1, k2) and torch.equal(v1, v2)
+
+
 def test_selective_validates_inputs(ct):
     g = golden("toy_cfg1")
     model = O.Model(O.ModelConfig(seed=0, n_layers=2))
