@@ -1268,7 +1268,10 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
               : poly == 0x2222 ? attention_pp_kernel<0x2222u> : attention_pp_kernel<0u>;
     int split = 1;
     if (const char* e = getenv("CT_TC_SPLIT")) split = atoi(e) == 2 ? 2 : 1;
-    if (split == 2) kp = poly == 0x4444 ? attention_pp_kernel<0x4444u, 1, 2, 4> : attention_pp_kernel<0u, 1, 2, 4>;
+    // split rows (neutral on the selective shape; the FMA-pipe polynomial in
+    // the key half of one warp set measured much slower,
+    // profiles/round1_attention_variants.md)
+    if (split == 2) kp = attention_pp_kernel<0u, 1, 2, 4>;
     const size_t smem_pp = (split == 2 ? SmemPP<4>::TOTAL : SmemPP<5>::TOTAL) + 1024;
     CT_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pp));
     const unsigned grid_pp = (unsigned)(((prm.n_qblocks + 1) / 2) * Hkv);
