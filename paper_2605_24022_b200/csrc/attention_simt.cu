@@ -6,6 +6,8 @@
 // core path lives in attention_tc.cu.
 #include "common.cuh"
 
+#include <stdlib.h>
+
 namespace ct {
 
 constexpr int AT_QB = 16;     // queries per CTA (4 per warp)
@@ -124,6 +126,239 @@ attention_simt_kernel(const T* __restrict__ q, const int32_t* __restrict__ qpos,
   }
 }
 
+// ---------------------------------------------------------------------------
+// Few-row path (split keys, "flash-decoding"): A x G <= DEC_MAXR rows, e.g.
+// the last layer's first-token row once the other rows are pruned
+// (prefill.run_layers).  A 32K-key scan by one CTA per kv head would leave
+// 140 SMs idle; instead block (s, g) scores a KEYS-wide key split of kv head g
+// for every row (thread per key), normalises locally and accumulates its
+// partial P V (thread per head-dim column), writing (O_s, m_s, l_s) to the
+// workspace; attention_decode_combine merges the splits in a fixed order
+// (deterministic).  Same mask / exp2 convention as the tensor-core kernel.
+constexpr int DEC_MAXR = 8;
+constexpr int DEC_THREADS = 128;
+
+inline int64_t decode_splits(int64_t n_ctx, int64_t Hkv) {
+  int64_t s = (2 * 148 + Hkv - 1) / Hkv;
+  const int64_t cap = (n_ctx + 255) / 256;        // >= 256 keys per split
+  if (s > cap) s = cap;
+  const int64_t need = (n_ctx + 2047) / 2048;      // <= 2048 keys (shared memory)
+  if (s < need) s = need;
+  return s < 1 ? 1 : s;
+}
+inline int64_t decode_keys(int64_t n_ctx, int64_t splits) {
+  return ((n_ctx + splits - 1) / splits + 31) / 32 * 32;
+}
+// 16-byte vectors along the head dim: D/VE chunks must tile the 128 threads
+inline bool decode_ok(int64_t A, int64_t Hq, int64_t Hkv, int64_t D, int dtype,
+                      const float* probs) {
+  const char* e = getenv("CT_ATT_DECODE");  // CT_ATT_DECODE=0: the full kernels at tiny A
+  if (probs || (e && atoi(e) == 0) || A * (Hq / Hkv) > DEC_MAXR) return false;
+  const int64_t ve = dtype == CT_BF16 ? 8 : 4;
+  return D % ve == 0 && DEC_THREADS % (D / ve) == 0;
+}
+inline size_t decode_workspace(int64_t A, int64_t Hq, int64_t n_ctx, int64_t Hkv, int64_t D) {
+  return (size_t)decode_splits(n_ctx, Hkv) * Hkv * A * (Hq / Hkv) * (D + 2) * sizeof(float);
+}
+
+inline bool cache_row_ok(const void* kc, const void* vc, int64_t crs, size_t esz) {
+  return !(((uintptr_t)kc | (uintptr_t)vc) & 15) && (crs * (int64_t)esz) % 16 == 0;
+}
+
+template <typename T>
+__device__ __forceinline__ void unpack_vec(const uint4& u, float* f);
+template <>
+__device__ __forceinline__ void unpack_vec<__nv_bfloat16>(const uint4& u, float* f) {
+  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xffff0000u);
+  }
+}
+template <>
+__device__ __forceinline__ void unpack_vec<float>(const uint4& u, float* f) {
+  f[0] = __uint_as_float(u.x);
+  f[1] = __uint_as_float(u.y);
+  f[2] = __uint_as_float(u.z);
+  f[3] = __uint_as_float(u.w);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(DEC_THREADS)
+attention_decode_partial(const T* __restrict__ q, const int32_t* __restrict__ qpos, int A, int Hq,
+                         const T* __restrict__ kc, const T* __restrict__ vc, int64_t n_ctx,
+                         int Hkv, int D, int64_t crs, float scale_log2, int keys,
+                         float* __restrict__ ws) {
+  constexpr int VE = 16 / sizeof(T);  // elements per 16-byte vector
+  extern __shared__ __align__(16) float dsm[];
+  const int G = Hq / Hkv, R = A * G;
+  const int CH = D / VE, KG = DEC_THREADS / CH;  // vector chunks per row, key groups
+  float* sq = dsm;                 // [R][D] queries (f32)
+  float* ss = sq + R * D;          // [R][keys] scores -> probabilities
+  float* red = ss + R * keys;      // [KG][R][D] partial O of the key groups
+  int* spos = reinterpret_cast<int*>(red + KG * R * D);
+  const int split = blockIdx.x, g = blockIdx.y, tid = threadIdx.x;
+  const int64_t k0 = (int64_t)split * keys;
+  const int nk = (int)max((int64_t)0, min(n_ctx, k0 + keys) - k0);
+  for (int t = tid; t < R * D; t += DEC_THREADS) {
+    const int r = t / D, d = t % D;
+    const int a = r / G, hj = r % G;
+    sq[t] = to_f32(q[((int64_t)a * Hq + g * G + hj) * D + d]);
+  }
+  for (int r = tid; r < R; r += DEC_THREADS)
+    spos[r] = (int)min((int64_t)qpos[r / G], n_ctx - 1);
+  __syncthreads();
+  // scores: one thread per key, the key row read as 16-byte vectors, 8 in flight
+  for (int j = tid; j < nk; j += DEC_THREADS) {
+    const uint4* krow = reinterpret_cast<const uint4*>(kc + (k0 + j) * crs + (int64_t)g * D);
+    float acc[DEC_MAXR];
+#pragma unroll
+    for (int r = 0; r < DEC_MAXR; ++r) acc[r] = 0.f;
+    for (int c0 = 0; c0 < CH; c0 += 8) {
+      uint4 u[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        if (c0 + i < CH) u[i] = __ldg(krow + c0 + i);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        if (c0 + i >= CH) break;
+        float f[VE];
+        unpack_vec<T>(u[i], f);
+        const int d0 = (c0 + i) * VE;
+#pragma unroll
+        for (int r = 0; r < DEC_MAXR; ++r) {
+          if (r >= R) break;
+#pragma unroll
+          for (int e = 0; e < VE; ++e) acc[r] = fmaf(sq[r * D + d0 + e], f[e], acc[r]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < DEC_MAXR; ++r)
+      if (r < R) ss[r * keys + j] = (k0 + j > spos[r]) ? -INFINITY : acc[r] * scale_log2;
+  }
+  __syncthreads();
+  // per-row max and probabilities: warp w owns rows w, w+4, ...
+  const int warp = tid / 32, lane = tid % 32;
+  float* wsb = ws + ((int64_t)split * Hkv + g) * R * (D + 2);
+  for (int r = warp; r < R; r += DEC_THREADS / 32) {
+    float m = -INFINITY;
+    for (int j = lane; j < nk; j += 32) m = fmaxf(m, ss[r * keys + j]);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    float l = 0.f;
+    for (int j = lane; j < nk; j += 32) {
+      const float pj = m == -INFINITY ? 0.f : exp2f(ss[r * keys + j] - m);
+      ss[r * keys + j] = pj;
+      l += pj;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane == 0) {
+      wsb[r * (D + 2) + D] = m;
+      wsb[r * (D + 2) + D + 1] = l;
+    }
+  }
+  __syncthreads();
+  // partial O = P V: thread (key group kg, chunk c) accumulates 16-byte
+  // column chunk c over keys kg, kg + KG, ... (4 rows in flight), then the key
+  // groups are summed through shared memory in a fixed order
+  {
+    const int c = tid % CH, kg = tid / CH;
+    float o[DEC_MAXR][VE];
+#pragma unroll
+    for (int r = 0; r < DEC_MAXR; ++r)
+#pragma unroll
+      for (int e = 0; e < VE; ++e) o[r][e] = 0.f;
+    const uint4* vbase = reinterpret_cast<const uint4*>(vc + k0 * crs + (int64_t)g * D) + c;
+    const int64_t vstride = crs / VE;  // uint4 per key row
+    for (int j0 = kg; j0 < nk; j0 += 4 * KG) {
+      uint4 u[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (j0 + i * KG < nk) u[i] = __ldg(vbase + (int64_t)(j0 + i * KG) * vstride);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int j = j0 + i * KG;
+        if (j >= nk) break;
+        float f[VE];
+        unpack_vec<T>(u[i], f);
+#pragma unroll
+        for (int r = 0; r < DEC_MAXR; ++r) {
+          if (r >= R) break;
+          const float pj = ss[r * keys + j];
+#pragma unroll
+          for (int e = 0; e < VE; ++e) o[r][e] = fmaf(pj, f[e], o[r][e]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < DEC_MAXR; ++r) {
+      if (r >= R) break;
+#pragma unroll
+      for (int e = 0; e < VE; ++e) red[(kg * R + r) * D + c * VE + e] = o[r][e];
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < R * D; t += DEC_THREADS) {
+    float acc = 0.f;
+    for (int kg = 0; kg < KG; ++kg) acc += red[kg * R * D + t];
+    wsb[(t / D) * (D + 2) + t % D] = acc;
+  }
+}
+
+template <typename TO>
+__global__ void attention_decode_combine(const float* __restrict__ ws, int A, int Hq, int Hkv,
+                                         int D, int splits, TO* __restrict__ out) {
+  const int G = Hq / Hkv, R = A * G;
+  const int r = blockIdx.x, g = blockIdx.y;
+  float M = -INFINITY;
+  for (int s = 0; s < splits; ++s)
+    M = fmaxf(M, ws[(((int64_t)s * Hkv + g) * R + r) * (D + 2) + D]);
+  float L = 0.f;
+  for (int s = 0; s < splits; ++s) {
+    const float* b = ws + (((int64_t)s * Hkv + g) * R + r) * (D + 2);
+    if (b[D] != -INFINITY) L += exp2f(b[D] - M) * b[D + 1];
+  }
+  const float inv = L > 0.f ? 1.f / L : 0.f;
+  const int a = r / G, hj = r % G;
+  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+    float acc = 0.f;
+    for (int s = 0; s < splits; ++s) {
+      const float* b = ws + (((int64_t)s * Hkv + g) * R + r) * (D + 2);
+      if (b[D] != -INFINITY) acc += exp2f(b[D] - M) * b[d];
+    }
+    out[((int64_t)a * Hq + g * G + hj) * D + d] = from_f32<TO>(acc * inv);
+  }
+}
+
+template <typename T, typename TO>
+int attention_decode(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, const void* kc,
+                     const void* vc, int64_t n_ctx, int64_t Hkv, int64_t D, int64_t crs,
+                     double scale, void* out, void* workspace, size_t workspace_bytes,
+                     cudaStream_t st) {
+  const int64_t splits = decode_splits(n_ctx, Hkv), keys = decode_keys(n_ctx, splits);
+  const int64_t R = A * (Hq / Hkv);
+  if (!workspace || workspace_bytes < decode_workspace(A, Hq, n_ctx, Hkv, D))
+    return fail(CT_ERR_PARAM, "attention workspace too small (%zu < %zu bytes)", workspace_bytes,
+                decode_workspace(A, Hq, n_ctx, Hkv, D));
+  const int64_t KG = DEC_THREADS / (D / (16 / (int64_t)sizeof(T)));
+  const size_t smem = (size_t)(R * D + R * keys + KG * R * D + R) * sizeof(float);
+  if (cache_row_ok(kc, vc, crs, sizeof(T)) == false)
+    return fail(CT_ERR_PARAM, "K/V caches must be 16-byte aligned with a 16-byte row stride");
+  auto kp = attention_decode_partial<T>;
+  CT_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kp<<<dim3((unsigned)splits, (unsigned)Hkv), DEC_THREADS, smem, st>>>(
+      (const T*)q, q_pos, (int)A, (int)Hq, (const T*)kc, (const T*)vc, n_ctx, (int)Hkv, (int)D,
+      crs, (float)(scale * 1.4426950408889634), (int)keys, (float*)workspace);
+  int rc = check_launch("attention_decode_partial");
+  if (rc) return rc;
+  attention_decode_combine<TO><<<dim3((unsigned)R, (unsigned)Hkv), 128, 0, st>>>(
+      (const float*)workspace, (int)A, (int)Hq, (int)Hkv, (int)D, (int)splits, (TO*)out);
+  return check_launch("attention_decode_combine");
+}
+
 int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, const void* k_cache,
                  const void* v_cache, int64_t n_ctx, int64_t Hkv, int64_t D,
                  int64_t cache_row_stride, double scale, void* out, int out_dtype,
@@ -137,6 +372,9 @@ using namespace ct;
 
 extern "C" size_t ct_attention_workspace_bytes(int64_t A, int64_t Hq, int64_t n_ctx, int64_t Hkv,
                                                int64_t D, int dtype) {
+  if (A > 0 && Hq >= Hkv && Hkv > 0 && Hq % Hkv == 0 && D > 0 &&
+      decode_ok(A, Hq, Hkv, D, dtype, nullptr))
+    return decode_workspace(A, Hq, n_ctx, Hkv, D);
   if (dtype == CT_BF16) return attention_tc_workspace(A, Hq, n_ctx, Hkv, D);
   return 0;
 }
@@ -154,6 +392,23 @@ extern "C" int ct_selective_attention(const void* q, const int32_t* q_pos, int64
   if (!valid_dtype(dtype) || !valid_dtype(out_dtype)) return fail(CT_ERR_PARAM, "dtype");
   if (A == 0) return CT_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (decode_ok(A, Hq, Hkv, D, dtype, probs)) {
+    if (dtype == CT_F32 && out_dtype == CT_F32)
+      return attention_decode<float, float>(q, q_pos, A, Hq, k_cache, v_cache, n_ctx, Hkv, D,
+                                            cache_row_stride, scale, out, workspace,
+                                            workspace_bytes, st);
+    if (dtype == CT_BF16 && out_dtype == CT_BF16)
+      return attention_decode<__nv_bfloat16, __nv_bfloat16>(
+          q, q_pos, A, Hq, k_cache, v_cache, n_ctx, Hkv, D, cache_row_stride, scale, out,
+          workspace, workspace_bytes, st);
+    if (dtype == CT_BF16)
+      return attention_decode<__nv_bfloat16, float>(q, q_pos, A, Hq, k_cache, v_cache, n_ctx,
+                                                    Hkv, D, cache_row_stride, scale, out,
+                                                    workspace, workspace_bytes, st);
+    return attention_decode<float, __nv_bfloat16>(q, q_pos, A, Hq, k_cache, v_cache, n_ctx, Hkv,
+                                                  D, cache_row_stride, scale, out, workspace,
+                                                  workspace_bytes, st);
+  }
   if (tc_enabled() && dtype == CT_BF16 && !probs && D == 128)
     return attention_tc(q, q_pos, A, Hq, k_cache, v_cache, n_ctx, Hkv, D, cache_row_stride, scale,
                         out, out_dtype, workspace, workspace_bytes, st);

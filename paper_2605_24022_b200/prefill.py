@@ -224,6 +224,9 @@ def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n
                 r0 = a - 1
         av = a - r0
         hv, xv, qv, ctxv, posv = buf.h[r0:], buf.x[r0:], buf.q[r0:], buf.ctx[r0:], positions[r0:]
+        if r0:  # few-row (split-key) attention: its own workspace
+            wsb = lib.ct_attention_workspace_bytes(av, hq, n_ctx, hkv, d, dtc)
+            ws = _dev.workspace(wsb, "attention_rows")
         probs = (torch.empty((hq, a, n_ctx), dtype=torch.float32, device=dev)
                  if record_attention else None)
         tname = "attention" if r0 == 0 else "attention_last_row"

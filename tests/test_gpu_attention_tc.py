@@ -26,9 +26,11 @@ def _run(q, pos, k, v, hq, hkv, out_dtype=torch.bfloat16):
     a, _, d = q.shape
     n = k.shape[0]
     out = torch.empty((a, hq, d), device="cuda", dtype=out_dtype)
+    wsb = _lib.load().ct_attention_workspace_bytes(a, hq, n, hkv, d, _lib.CT_BF16)
+    ws = _dev.workspace(wsb, "test_attention")
     _lib.call("ct_selective_attention", _dev.ptr(q), _dev.ptr(pos), a, hq, _dev.ptr(k),
               _dev.ptr(v), n, hkv, d, k.stride(0), 1.0 / d ** 0.5, _lib.CT_BF16, _dev.ptr(out),
-              _dev.ct_dtype(out_dtype), None, None, 0, _dev.stream_handle())
+              _dev.ct_dtype(out_dtype), None, _dev.ptr(ws), wsb, _dev.stream_handle())
     torch.cuda.synchronize()
     return out
 
@@ -126,3 +128,34 @@ def test_tc_attention_randomised_geometries_deterministic():
         mod.main()
     finally:
         sys.argv = argv
+
+
+@pytest.mark.parametrize("a,hq,hkv,n,out_dtype", [
+    (1, 32, 8, 32832, torch.bfloat16),   # the last-layer first-token row at config-2 size
+    (1, 32, 8, 1, torch.bfloat16),       # one key
+    (2, 8, 2, 5000, torch.float32),      # 8 rows (the path's limit), f32 output
+    (3, 8, 8, 100, torch.bfloat16),      # MHA, fewer keys than one split
+    (4, 16, 4, 70000, torch.bfloat16),   # more than 2048 keys per split needed -> more splits
+])
+def test_few_row_split_key_attention(monkeypatch, a, hq, hkv, n, out_dtype):
+    """A x G <= 8 rows take the split-key path (ct_selective_attention picks it;
+    the caller sizes the workspace with ct_attention_workspace_bytes); it must
+    agree with the fp32 reference and, for D = 128 bf16, with the tcgen05
+    kernel forced on the same rows (CT_ATT_DECODE=0), and be deterministic."""
+    gen = torch.Generator(device="cuda").manual_seed(a * 7 + n)
+    d = 128
+    q = torch.randn((a, hq, d), device="cuda", generator=gen).to(torch.bfloat16)
+    k = torch.randn((n, hkv, d), device="cuda", generator=gen).to(torch.bfloat16)
+    v = torch.randn((n, hkv, d), device="cuda", generator=gen).to(torch.bfloat16)
+    pos = torch.sort(torch.randperm(n, device="cuda", generator=gen)[:a])[0].to(torch.int32)
+    pos[-1] = n - 1
+    out = _run(q, pos, k, v, hq, hkv, out_dtype)
+    again = _run(q, pos, k, v, hq, hkv, out_dtype)
+    assert torch.equal(out, again)
+    want = _ref(q, pos, k, v, hq, hkv)
+    err = (out.float() - want).abs().max().item() / want.abs().max().item()
+    assert err < 5e-3, err
+    monkeypatch.setenv("CT_ATT_DECODE", "0")
+    tc = _run(q, pos, k, v, hq, hkv, out_dtype)
+    err_tc = (tc.float() - want).abs().max().item() / want.abs().max().item()
+    assert err_tc < 1e-2, err_tc

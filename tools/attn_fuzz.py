@@ -57,9 +57,11 @@ def main():
         outs = []
         for _ in range(2):
             out = torch.empty_like(q)
+            wsb = _lib.load().ct_attention_workspace_bytes(a, hq, n, hkv, 128, _lib.CT_BF16)
+            ws = _dev.workspace(wsb, "fuzz")
             _lib.call("ct_selective_attention", _dev.ptr(q), _dev.ptr(p), a, hq, _dev.ptr(k),
                       _dev.ptr(v), n, hkv, 128, hkv * 128, 1 / 128 ** 0.5, _lib.CT_BF16,
-                      _dev.ptr(out), _lib.CT_BF16, None, None, 0, _dev.stream_handle())
+                      _dev.ptr(out), _lib.CT_BF16, None, _dev.ptr(ws), wsb, _dev.stream_handle())
             torch.cuda.synchronize()
             outs.append(out)
         assert torch.equal(outs[0], outs[1]), f"case {c}: non-deterministic"
