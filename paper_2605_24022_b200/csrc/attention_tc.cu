@@ -986,6 +986,13 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
       mbar_wait(bar_sfull(x), (uint32_t)(j & 1));
       __syncwarp();
       tc_fence_after();
+      if constexpr (SCHED == 4) {  // timing probe (wrong values): MMA + TMA pipeline alone
+        l = 1.f;
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar_pfull(x));
+        continue;
+      }
 #pragma unroll
       for (int c = 0; c < KEYS / 32; ++c) tmem_ld32(tS(x) + lane_off + col0 + c * 32, r + c * 32);
 #pragma unroll
@@ -1258,6 +1265,7 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
     if (const char* e = getenv("CT_TC_SCHED")) sched = atoi(e);
     KernFn kp = sched == 0 ? (poly == 0x4444 ? attention_pp_kernel<0x4444u, 0> : attention_pp_kernel<0u, 0>)
               : sched == 3 ? attention_pp_kernel<0u, 3>
+              : sched == 4 ? attention_pp_kernel<0u, 4>
               : poly == 0x3333 ? attention_pp_kernel<0x3333u>
               : poly == 0x7777 ? attention_pp_kernel<0x7777u>
               : poly == 0xFFFF ? attention_pp_kernel<0xFFFFu>
