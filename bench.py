@@ -48,6 +48,12 @@ CONFIGS = {
                       "65600-token context, r=0.15",
                  arch="mistral_7b", layers=32, vocab=32768, chunks=32, chunk_tokens=2048,
                  suffix=64, r=0.15),
+    "cfg5": dict(desc="config 5: batch of 64 independent RAG requests, each 16 chunks x 2048 "
+                      "tokens drawn from a shared 64-chunk importance-ordered KV corpus resident "
+                      "in HBM (Llama-3-8B geometry) + its own 64-token suffix, r=0.15; request i "
+                      "-> rank i mod N (strong scaling: the batch is fixed)",
+                 arch="llama3_8b", layers=32, vocab=128256, chunks=16, chunk_tokens=2048,
+                 suffix=64, r=0.15, corpus=64, requests=64),
     "small": dict(desc="reduced smoke workload: Llama-3-8B layer geometry, 2 layers, "
                        "4 chunks x 2048 + 64", arch="llama3_8b", layers=2, vocab=8192,
                   chunks=4, chunk_tokens=2048, suffix=64, r=0.15),
@@ -488,6 +494,140 @@ def run_ours(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_batch(args, rank, world, local_rank):
+    """Config 5: one step = the whole batch of independent requests, sharded
+    i -> rank i mod N with no collective on the hot path.  Every rank holds a
+    replica of the model and of the shared chunk corpus (its importance-ordered
+    KV pool in HBM); a request binds its 16 documents and runs the online path.
+    value = batch requests / max-over-ranks step time; e2e = the same with each
+    request's suffix tokens and chunk ids from pinned host memory and its
+    first-token logits back to pinned host memory inside the timed region."""
+    import torch
+    import torch.distributed as dist
+    import paper_2605_24022_b200 as ct
+    from paper_2605_24022_b200 import _lib
+    from paper_2605_24022_b200.distributed import RequestResult, gather_results, shard_requests
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+
+    c = CONFIGS[args.config]
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
+    arch = getattr(ct.ModelConfig, c["arch"])
+    cfg = arch(n_layers=c["layers"], vocab_size=c["vocab"], seed=1234)
+    t0 = time.time()
+    model = ct.GpuModel.random(cfg, dtype=torch.bfloat16, device=dev)
+    corpus = []
+    for j in range(c["corpus"]):  # same corpus on every rank (document seeds)
+        toks = np.random.default_rng([j, 5]).integers(0, cfg.vocab_size, size=c["chunk_tokens"])
+        corpus.append(ct.encode_chunk_isolated(model, toks, chunk_id=f"doc{j}"))
+    ranks = ct.rank_chunks(corpus)
+    pool = KvPool(corpus, ranks, "hbm", device=dev)
+    del corpus
+    torch.cuda.empty_cache()
+    torch.cuda.synchronize()
+    log(f"[bench] corpus of {c['corpus']} chunks encoded, ranked, pooled {time.time() - t0:.1f}s")
+    mine = shard_requests(c["requests"], rank, world)
+    reqs = {}
+    for i in mine:
+        rng = np.random.default_rng([i, 11])
+        docs = [int(x) for x in rng.choice(c["corpus"], size=c["chunks"], replace=False)]
+        suf = rng.integers(0, cfg.vocab_size, size=c["suffix"]).astype(np.int32)
+        reqs[i] = (docs, torch.as_tensor(suf, device=dev), torch.as_tensor(suf).pin_memory())
+    eng = SelectivePrefillEngine(model, pool, c["r"], c["suffix"], n_chunks=c["chunks"])
+    logits_host = {i: torch.empty((1, cfg.vocab_size), dtype=torch.float32).pin_memory()
+                   for i in mine}
+
+    def batch(e2e=False, out=None):
+        for i in mine:
+            docs, sd, sh = reqs[i]
+            eng.bind(docs)
+            if e2e:
+                eng.step(sh, logits_host[i])
+            else:
+                lg = eng.step(sd)
+                if out is not None:
+                    out[i] = lg
+    for _ in range(args.warmup):
+        batch()
+    torch.cuda.synchronize()
+
+    def timed(fn):
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        for _ in range(args.steps):
+            fn()
+        e.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        return s.elapsed_time(e)
+
+    req_ms = []
+    launches0 = _lib.LAUNCH_COUNT["n"]
+    with ClockSampler(local_rank) as clk:
+        total = timed(batch)
+    launches = _lib.LAUNCH_COUNT["n"] - launches0
+    e2e_total = timed(lambda: batch(e2e=True))
+    # per-request TTFT (after the timed regions)
+    last = {}
+    for i in mine:
+        docs, sd, _ = reqs[i]
+        eng.bind(docs)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        last[i] = eng.step(sd)
+        e.record()
+        torch.cuda.synchronize()
+        req_ms.append(s.elapsed_time(e))
+    g0 = time.perf_counter()
+    gathered = gather_results([RequestResult(i, req_ms[j], last[i][0].float(),
+                                             eng.positions[:eng.n_rec].clone())
+                               for j, i in enumerate(mine)], cfg.vocab_size, eng.n_rec, device=dev)
+    gather_ms = (time.perf_counter() - g0) * 1e3
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+    total, e2e_total = allmax(total), allmax(e2e_total)
+    p50 = allmax(statistics.median(req_ms))
+    if rank != 0:
+        return
+    n_req = c["requests"]
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
+        cpu = {"value": 1.0 / sec, "unit": "requests/s", "cores": cpu_threads(), "kind": "port",
+               "sample": desc}
+    line = {
+        "metric": METRIC, "value": n_req * args.steps / (total * 1e-3), "unit": "requests/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total / args.steps, "p50_ttft_ms": p50, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, seeded document and suffix token ids; corpus KV "
+                "encoded on the GPU by the same model)",
+        "config": {"workload": c["desc"], "parallelism": f"replicas x{world} (request-level)",
+                   "requests_per_step": n_req, "requests_on_rank0": len(mine),
+                   "l2": "inputs larger than L2 (17 GB corpus + 16 GB weights); no flush"},
+        "e2e": {"value": n_req * args.steps / (e2e_total * 1e-3), "unit": "requests/s",
+                "h2d_bytes_per_step": n_req * 4 * (c["suffix"] + c["chunks"]),
+                "d2h_bytes_per_step": n_req * 4 * cfg.vocab_size},
+        "gpu_launches": launches,
+        "result_gather": {"requests": len(gathered) if gathered else 0, "ms": gather_ms},
+        "clocks": clk.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -511,7 +651,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if "requests" in CONFIGS[args.config]:
+            run_batch(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -183,7 +183,11 @@ int ct_gather_rows(const void* src, const int32_t* idx, int64_t n,
  * [Hq][A][n_ctx]) receives the normalised attention matrix (AttentionRecord,
  * ct/toymodel.py:92-110).
  * dtype CT_F32: SIMT fp32 path (1e-5 mode).  dtype CT_BF16: tcgen05/TMEM
- * path on sm_100a (bf16 operands, fp32 accumulation), D == 128. */
+ * path on sm_100a (bf16 operands, fp32 accumulation), D == 128.
+ * A * (Hq/Hkv) <= 8 rows without probs (e.g. a first-token row alone): the
+ * split-key path (key range split over ~2 CTAs per SM, fixed-order combine);
+ * it needs ct_attention_workspace_bytes(...) of workspace (0 otherwise) and
+ * returns CT_ERR_PARAM when the workspace is missing or short. */
 size_t ct_attention_workspace_bytes(int64_t A, int64_t Hq, int64_t n_ctx,
                                     int64_t Hkv, int64_t D, int dtype);
 int ct_selective_attention(const void* q, const int32_t* q_pos, int64_t A,

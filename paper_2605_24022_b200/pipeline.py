@@ -65,15 +65,26 @@ class KernelTimer:
 
 
 class SelectivePrefillEngine:
+    """One request at a time: the context is `n_chunks` chunks of the pool (by
+    default all of them, in pool order) + a suffix of `suffix_len` tokens.
+    With a corpus pool (more chunks than a request uses) `bind(chunk_ids)`
+    points the engine at the request's chunks -- RAG requests drawing
+    different documents from one shared, importance-ordered KV corpus -- and
+    reuses every device buffer."""
+
     def __init__(self, model: GpuModel, pool: KvPool, r: float, suffix_len: int,
-                 timer: KernelTimer | None = None):
+                 timer: KernelTimer | None = None, n_chunks: int | None = None):
         cfg = model.config
         if (pool.L, pool.H, pool.D) != (cfg.n_layers, cfg.kv_heads, cfg.head_dim):
             raise ValueError("pool geometry disagrees with model")
         self.model, self.pool, self.r, self.S = model, pool, r, suffix_len
         self.timer = timer or KernelTimer()
         dev = model.device
-        C, N, L, H, D = pool.C, pool.N, pool.L, pool.H, pool.D
+        C = pool.C if n_chunks is None else int(n_chunks)
+        if not 1 <= C <= pool.C:
+            raise ValueError(f"a request uses 1..{pool.C} chunks of this pool, not {C}")
+        N, L, H, D = pool.N, pool.L, pool.H, pool.D
+        self.C = C
         self.k = selection_count(r, N)
         self.n_keep = N - self.k
         self.history = C * N
@@ -97,40 +108,64 @@ class SelectivePrefillEngine:
         self.table = rope_table(cfg.rope_params, self.n_ctx, "f64" if dt == torch.float32
                                 else "f32", dev)
         self.pinned = pool.location == "pinned"
-        row = pool.row_bytes
         self.row_elems = H * D
         if self.pinned:
             self.stage = torch.empty((L, C, max(self.n_keep, 1), 2, H, D), dtype=dt, device=dev)
             self.copy_stream = torch.cuda.Stream(device=dev)
             self.copy_done = [torch.cuda.Event() for _ in range(L)]
             self.step_start = torch.cuda.Event()
-            nbytes = self.n_keep * 2 * row
-            self.copy_args = []
-            for l in range(L):
-                dst = [self.stage[l, c].data_ptr() for c in range(C)]
-                src = [pool.tail_ptr(c, l, self.k) for c in range(C)]
-                self.copy_args.append(((ctypes.c_void_p * C)(*dst), (ctypes.c_void_p * C)(*src),
-                                       (ctypes.c_int64 * C)(*([nbytes] * C))))
-            self.h2d_bytes = L * C * nbytes
+            self.h2d_bytes = L * C * self.n_keep * 2 * pool.row_bytes
         else:
             self.h2d_bytes = 0
-        # per-layer K3 segments (kernel parameters, built once)
-        esz = pool.esize
-        self.segs = []
-        for l in range(L):
-            segs = []
-            for c in range(C):
-                if self.n_keep == 0:
-                    continue
-                base = self.stage[l, c].data_ptr() if self.pinned else pool.tail_ptr(c, l, self.k)
-                tok = pool.agg.data_ptr() + (c * N + self.k) * 4
-                segs.append(_lib.Segment(base, base + H * D * esz, tok, self.n_keep, c * N, 0))
-            self.segs.append((_lib.Segment * max(len(segs), 1))(*segs) if segs else None)
         self.n_segs = C if self.n_keep else 0
         self.launches_per_step = None
         self.record_timeline = False
         self._events: dict = {}
         self.graph = None
+        # the request's chunks: aggregate orders and token ids gathered from
+        # the pool (device), transfer / blend parameters built on the host
+        self.agg = torch.empty((C, N), dtype=torch.int32, device=dev)
+        self.chunk_tokens = torch.empty((C, N), dtype=torch.int32, device=dev)
+        self.chunk_ids = None
+        self.bind(list(range(C)))
+
+    def bind(self, chunk_ids) -> None:
+        """Point the engine at pool chunks `chunk_ids` (len == n_chunks, pool
+        indices or ids), in context order.  Asynchronous on the current stream;
+        not allowed while a captured graph is in use (its parameters are baked)."""
+        pool, C, N = self.pool, self.C, self.pool.N
+        idx = [pool.chunk_index(c) for c in chunk_ids]
+        if len(idx) != C:
+            raise ValueError(f"request needs exactly {C} chunks, got {len(idx)}")
+        if self.graph is not None and idx != self.chunk_ids:
+            raise RuntimeError("bind() would change a captured graph's parameters")
+        self.chunk_ids = idx
+        # pinned + non_blocking: binding the next request never waits for the
+        # GPU to drain the current one
+        sel = torch.tensor(idx, dtype=torch.long).pin_memory().to(self.agg.device,
+                                                                  non_blocking=True)
+        torch.index_select(pool.agg, 0, sel, out=self.agg)
+        torch.index_select(pool.tokens, 0, sel, out=self.chunk_tokens)
+        L, H, D, esz = pool.L, pool.H, pool.D, pool.esize
+        if self.pinned:
+            nbytes = self.n_keep * 2 * pool.row_bytes
+            self.copy_args = []
+            for l in range(L):
+                dst = [self.stage[l, c].data_ptr() for c in range(C)]
+                src = [pool.tail_ptr(ci, l, self.k) for ci in idx]
+                self.copy_args.append(((ctypes.c_void_p * C)(*dst), (ctypes.c_void_p * C)(*src),
+                                       (ctypes.c_int64 * C)(*([nbytes] * C))))
+        # per-layer K3 segments (kernel parameters)
+        self.segs = []
+        for l in range(L):
+            segs = []
+            for c, ci in enumerate(idx):
+                if self.n_keep == 0:
+                    continue
+                base = self.stage[l, c].data_ptr() if self.pinned else pool.tail_ptr(ci, l, self.k)
+                tok = self.agg.data_ptr() + (c * N + self.k) * 4
+                segs.append(_lib.Segment(base, base + H * D * esz, tok, self.n_keep, c * N, 0))
+            self.segs.append((_lib.Segment * max(len(segs), 1))(*segs) if segs else None)
 
     # real three-stream timeline (ct/pipesim.py Timeline schema) ------------------
     def _ev(self, stream: str, layer: int, edge: int) -> torch.cuda.Event:
@@ -179,7 +214,7 @@ class SelectivePrefillEngine:
 
     def blend_bytes_per_layer(self) -> int:
         # read keep rows (K and V) + write them into the cache
-        return 2 * 2 * self.pool.C * self.n_keep * self.pool.row_bytes
+        return 2 * 2 * self.C * self.n_keep * self.pool.row_bytes
 
     def _reuse(self, l: int) -> None:
         if self.n_segs == 0:
@@ -200,7 +235,7 @@ class SelectivePrefillEngine:
     def step(self, suffix=None, logits_out: torch.Tensor | None = None) -> torch.Tensor:
         """One request: suffix (host pinned or device int32 [S]) -> last-row logits."""
         pool, st = self.pool, _dev.stream_handle()
-        C, N = pool.C, pool.N
+        C, N = self.C, pool.N
         if self.record_timeline:
             self._ev("step", 0, 0).record()
         if self.pinned:
@@ -219,12 +254,12 @@ class SelectivePrefillEngine:
         if suffix is not None and self.S:
             self.tokens[self.n_rec:].copy_(suffix, non_blocking=True)
         m = self.meta
-        _lib.call("ct_selection_plan", _dev.ptr(pool.agg), _dev.ptr(m[:C + 1]),
+        _lib.call("ct_selection_plan", _dev.ptr(self.agg), _dev.ptr(m[:C + 1]),
                   _dev.ptr(m[C + 1:2 * C + 1]), _dev.ptr(m[2 * C + 1:3 * C + 2]),
                   _dev.ptr(m[3 * C + 2:]), C, N, _dev.ptr(self.positions), _dev.ptr(self.keep),
                   _dev.ptr(self.keep_src), st)
         if self.n_rec:
-            _lib.call("ct_gather_rows", _dev.ptr(pool.tokens), _dev.ptr(self.positions),
+            _lib.call("ct_gather_rows", _dev.ptr(self.chunk_tokens), _dev.ptr(self.positions),
                       self.n_rec, 4, _dev.ptr(self.tokens), st)
         logits, _ = run_layers(self.model, self.tokens, self.positions, self.n_ctx, self.caches,
                                reuse=self._reuse, logits_rows="last", buffers=self.buffers,

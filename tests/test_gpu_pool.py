@@ -70,6 +70,36 @@ def test_engine_hbm_and_pinned_pools_agree(ct):
     assert torch.equal(ref.logits.float().cpu(), outs[0])
 
 
+@pytest.mark.parametrize("location", ["hbm", "pinned"])
+def test_corpus_pool_requests_match_dedicated_pools(ct, location):
+    """Config-5 style serving: one importance-ordered corpus pool, each request
+    binds a different subset of its chunks (in its own order).  Logits and the
+    blended cache equal those of an engine over a pool built from exactly the
+    request's chunks, bit for bit, and rebinding between requests is clean."""
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=1024, seed=6)
+    m = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(6)
+    chunks = [ct.encode_chunk_isolated(m, rng.integers(0, 1024, size=512), chunk_id=f"d{j}")
+              for j in range(5)]
+    ranks = ct.rank_chunks(chunks)
+    corpus = KvPool(chunks, ranks, location)
+    eng = SelectivePrefillEngine(m, corpus, 0.15, 16, n_chunks=3)
+    suffix = torch.as_tensor(rng.integers(0, 1024, size=16).astype(np.int32), device="cuda")
+    for req in ([4, 1, 2], ["d0", "d3", "d1"], [4, 1, 2]):
+        eng.bind(req)
+        got = eng.step(suffix).float().cpu()
+        got_cache = eng.cache.float().cpu()
+        idx = [corpus.chunk_index(c) for c in req]
+        own = SelectivePrefillEngine(m, KvPool([chunks[i] for i in idx], [ranks[i] for i in idx],
+                                               location), 0.15, 16)
+        assert torch.equal(got, own.step(suffix).float().cpu())
+        assert torch.equal(got_cache, own.cache.float().cpu())
+    with pytest.raises(ValueError):
+        eng.bind([0, 1])
+
+
 def test_real_three_stream_timeline_audited(ct):
     """CUDA-event timeline of a pinned-pool request in the simulator's schema
     (ct/pipesim.py:93-105), checked with validate_timeline (ct/pipesim.py:257-279):
