@@ -492,6 +492,12 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
   load_tile<IN, N, TW, THREADS>(tile, base, ld_token, lane0, lane_end, vec_ok);
   cp_async_wait_all();
   __syncthreads();
+  // per-thread energies of tokens t + GT r over this thread's signals, in a
+  // fixed order (its signals, tile by tile); the groups are merged once at
+  // the end in group order
+  double eacc[16];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) eacc[r] = 0.0;
   for (int it = 0; it < iters; ++it) {
     cpx<T> v[SPT][16];
     // f1 input: lanes (2 sig, 2 sig + 1) of tokens t + GT r
@@ -604,24 +610,21 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
       }
       dft16<true>(v[s]);
     }
-    // energies -> the signals' (now free) exchange buffers, then one barrier
-    // and acc[n] += e_0[n] + e_1[n] + ... in signal order (fixed, deterministic)
-    group_sync<GT>(g);
 #pragma unroll
-    for (int s = 0; s < SPT; ++s) {
-      double* eb = reinterpret_cast<double*>(sigs[s]);
+    for (int s = 0; s < SPT; ++s)
 #pragma unroll
       for (int r = 0; r < 16; ++r)
-        eb[t + GT * r] = (double)(v[s][r].x * v[s][r].x + v[s][r].y * v[s][r].y);
-    }
-    cp_async_wait_all();  // next tile landed; the barrier publishes it too
+        eacc[r] += (double)(v[s][r].x * v[s][r].x + v[s][r].y * v[s][r].y);
+    cp_async_wait_all();  // next tile landed; the barrier publishes it (and frees sig)
     __syncthreads();
-    for (int n = threadIdx.x; n < N; n += THREADS) {
-      double a_n = acc[n];
+  }
+  // merge the groups' energies in group order (deterministic)
+  for (int gg = 0; gg < Cfg::NG; ++gg) {
+    if (g == gg) {
 #pragma unroll
-      for (int q = 0; q < NS; ++q) a_n += reinterpret_cast<const double*>(sigall + q * Cfg::SIGPAD)[n];
-      acc[n] = a_n;
+      for (int r = 0; r < 16; ++r) acc[t + GT * r] += eacc[r];
     }
+    __syncthreads();
   }
   const double inv_n2 = 1.0 / ((double)N * (double)N);
   const int nlb = gridDim.x;
