@@ -139,7 +139,7 @@ constexpr int DEC_MAXR = 8;
 constexpr int DEC_THREADS = 128;
 
 inline int64_t decode_splits(int64_t n_ctx, int64_t Hkv) {
-  int64_t s = (2 * 148 + Hkv - 1) / Hkv;
+  int64_t s = (6 * 148 + Hkv - 1) / Hkv;          // ~6 CTAs per SM: loads in flight
   const int64_t cap = (n_ctx + 255) / 256;        // >= 256 keys per split
   if (s > cap) s = cap;
   const int64_t need = (n_ctx + 2047) / 2048;      // <= 2048 keys (shared memory)
@@ -308,27 +308,56 @@ attention_decode_partial(const T* __restrict__ q, const int32_t* __restrict__ qp
   }
 }
 
+// One block per (row, kv head), 128 threads: split maxima and weights by a
+// fixed-shape block reduction, then thread-per-column weighted sums over the
+// splits (coalesced along the head dim, 8 loads in flight).  Deterministic.
 template <typename TO>
-__global__ void attention_decode_combine(const float* __restrict__ ws, int A, int Hq, int Hkv,
-                                         int D, int splits, TO* __restrict__ out) {
+__global__ void __launch_bounds__(DEC_THREADS)
+attention_decode_combine(const float* __restrict__ ws, int A, int Hq, int Hkv, int D, int splits,
+                         TO* __restrict__ out) {
+  extern __shared__ float cw[];  // [splits] weights 2^(m_s - M)
+  __shared__ float red[DEC_THREADS / 32];
   const int G = Hq / Hkv, R = A * G;
-  const int r = blockIdx.x, g = blockIdx.y;
-  float M = -INFINITY;
-  for (int s = 0; s < splits; ++s)
-    M = fmaxf(M, ws[(((int64_t)s * Hkv + g) * R + r) * (D + 2) + D]);
-  float L = 0.f;
-  for (int s = 0; s < splits; ++s) {
-    const float* b = ws + (((int64_t)s * Hkv + g) * R + r) * (D + 2);
-    if (b[D] != -INFINITY) L += exp2f(b[D] - M) * b[D + 1];
+  const int r = blockIdx.x, g = blockIdx.y, tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int64_t stride = (int64_t)Hkv * R * (D + 2);
+  const float* b0 = ws + ((int64_t)g * R + r) * (D + 2);
+  float m = -INFINITY;
+  for (int sp = tid; sp < splits; sp += DEC_THREADS) m = fmaxf(m, b0[sp * stride + D]);
+#pragma unroll
+  for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red[warp] = m;
+  __syncthreads();
+  float M = red[0];
+#pragma unroll
+  for (int w = 1; w < DEC_THREADS / 32; ++w) M = fmaxf(M, red[w]);
+  __syncthreads();
+  float lsum = 0.f;
+  for (int sp = tid; sp < splits; sp += DEC_THREADS) {
+    const float ms = b0[sp * stride + D];
+    const float w = ms == -INFINITY ? 0.f : exp2f(ms - M);
+    cw[sp] = w;
+    lsum += w * b0[sp * stride + D + 1];
   }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+  if (lane == 0) red[warp] = lsum;
+  __syncthreads();
+  float L = 0.f;
+#pragma unroll
+  for (int w = 0; w < DEC_THREADS / 32; ++w) L += red[w];
   const float inv = L > 0.f ? 1.f / L : 0.f;
   const int a = r / G, hj = r % G;
-  for (int d = threadIdx.x; d < D; d += blockDim.x) {
+  for (int d = tid; d < D; d += DEC_THREADS) {
     float acc = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const float* b = ws + (((int64_t)s * Hkv + g) * R + r) * (D + 2);
-      if (b[D] != -INFINITY) acc += exp2f(b[D] - M) * b[d];
+    int sp = 0;
+    for (; sp + 8 <= splits; sp += 8) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = b0[(sp + u) * stride + d];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) acc = fmaf(cw[sp + u], v[u], acc);
     }
+    for (; sp < splits; ++sp) acc = fmaf(cw[sp], b0[sp * stride + d], acc);
     out[((int64_t)a * Hq + g * G + hj) * D + d] = from_f32<TO>(acc * inv);
   }
 }
@@ -354,7 +383,8 @@ int attention_decode(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq,
       crs, (float)(scale * 1.4426950408889634), (int)keys, (float*)workspace);
   int rc = check_launch("attention_decode_partial");
   if (rc) return rc;
-  attention_decode_combine<TO><<<dim3((unsigned)R, (unsigned)Hkv), 128, 0, st>>>(
+  attention_decode_combine<TO><<<dim3((unsigned)R, (unsigned)Hkv), DEC_THREADS,
+                                 (size_t)splits * sizeof(float), st>>>(
       (const float*)workspace, (int)A, (int)Hq, (int)Hkv, (int)D, (int)splits, (TO*)out);
   return check_launch("attention_decode_combine");
 }

@@ -25,6 +25,8 @@ def main():
     ap.add_argument("--qscale", type=float, default=1.0)
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--rows", type=int, default=0,
+                    help="only the last ROWS query rows (the few-row split-key path)")
     args = ap.parse_args()
     hq, hkv, d = 32, 8, 128
     rng = np.random.default_rng(0)
@@ -35,6 +37,8 @@ def main():
         pos = np.concatenate([np.sort(rng.choice(2048, 308, replace=False)) + c * 2048
                               for c in range(16)] + [np.arange(32768, 32832)])
         n = 32832
+    if args.rows:
+        pos = pos[-args.rows:]
     a = pos.size
     gen = torch.Generator(device="cuda").manual_seed(0)
     q = (args.qscale * torch.randn((a, hq, d), device="cuda", generator=gen)).to(torch.bfloat16)
@@ -44,10 +48,13 @@ def main():
     out = torch.empty_like(q)
     flops = 4.0 * hq * d * float(np.sum(pos + 1.0))
 
+    wsb = _lib.load().ct_attention_workspace_bytes(a, hq, n, hkv, d, _lib.CT_BF16)
+    ws = _dev.workspace(wsb, "bench")
+
     def run():
         _lib.call("ct_selective_attention", _dev.ptr(q), _dev.ptr(p), a, hq, _dev.ptr(k),
                   _dev.ptr(v), n, hkv, d, hkv * d, 1 / d ** 0.5, _lib.CT_BF16, _dev.ptr(out),
-                  _lib.CT_BF16, None, None, 0, _dev.stream_handle())
+                  _lib.CT_BF16, None, _dev.ptr(ws), wsb, _dev.stream_handle())
     for _ in range(3):
         run()
     torch.cuda.synchronize()
@@ -58,8 +65,9 @@ def main():
     e.record()
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.iters
+    kv_gbs = 2 * n * hkv * d * 2 / ms / 1e6
     print(f"attention {'full' if args.full else 'selective'} A={a} n_ctx={n} qscale={args.qscale}: "
-          f"{ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s")
+          f"{ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s  (K+V once: {kv_gbs:.0f} GB/s)")
 
 
 if __name__ == "__main__":
