@@ -209,16 +209,28 @@ def cpu_threads() -> int:
         return os.cpu_count() or 1
 
 
+def all_host_threads():
+    """BLAS thread pool sized to every host core this process may use (torchrun
+    exports OMP_NUM_THREADS=1, which numpy's OpenBLAS would otherwise honour)."""
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=cpu_threads())
+    except ImportError:  # pragma: no cover
+        import contextlib
+        return contextlib.nullcontext()
+
+
 def run_reference(args, rank, world):
     c = CONFIGS[args.config]
     if rank != 0:
         return
     times = []
     desc = ""
-    for i in range(args.warmup + args.steps):
-        s, desc = cpu_sample(args.config, seed=i, rows=args.cpu_rows)
-        if i >= args.warmup:
-            times.append(s)
+    with all_host_threads():
+        for i in range(args.warmup + args.steps):
+            s, desc = cpu_sample(args.config, seed=i, rows=args.cpu_rows)
+            if i >= args.warmup:
+                times.append(s)
     sec = statistics.median(times)
     val = 1.0 / sec
     line = {
@@ -431,7 +443,8 @@ def run_ours(args, rank, world, local_rank):
 
     cpu = None
     if world == 1 and not args.no_cpu:
-        sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
+        with all_host_threads():
+            sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
         cpu = {"value": 1.0 / sec, "unit": "requests/s", "cores": cpu_threads(), "kind": "port",
                "sample": desc}
     line = {
@@ -604,7 +617,8 @@ def run_batch(args, rank, world, local_rank):
     n_req = c["requests"]
     cpu = None
     if world == 1 and not args.no_cpu:
-        sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
+        with all_host_threads():
+            sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
         cpu = {"value": 1.0 / sec, "unit": "requests/s", "cores": cpu_threads(), "kind": "port",
                "sample": desc}
     line = {
@@ -648,8 +662,16 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as dist
+        # CT_BENCH_DIST=gloo + ranks folded onto the visible GPUs: a functional
+        # check of the multi-rank path on a one-GPU box (its timings mean nothing)
+        backend = os.environ.get("CT_BENCH_DIST", "nccl")
+        if backend != "nccl":
+            local_rank %= torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         if "requests" in CONFIGS[args.config]:
             run_batch(args, rank, world, local_rank)
