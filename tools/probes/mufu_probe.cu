@@ -45,6 +45,37 @@ __global__ void k_bf16x2(float* out, float seed) {
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+__global__ void k_ffma(float* out, float seed) {
+  float x[CH];
+  for (int c = 0; c < CH; ++c) x[c] = seed * (threadIdx.x + c) * 1e-6f;
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) asm volatile("fma.rn.f32 %0, %0, 0f3F7FFFFF, 0f3A800000;" : "+f"(x[c]));
+  float s = 0;
+  for (int c = 0; c < CH; ++c) s += x[c];
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+__global__ void k_ffma2(float* out, float seed) {
+  unsigned long long x[CH];
+  for (int c = 0; c < CH; ++c) {
+    float a = seed * (threadIdx.x + c) * 1e-6f;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(x[c]) : "f"(a), "f"(a));
+  }
+  unsigned long long m, k;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(m) : "f"(0.99999994f), "f"(0.99999994f));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(k) : "f"(0.0009765625f), "f"(0.0009765625f));
+  for (int i = 0; i < ITERS; ++i)
+#pragma unroll
+    for (int c = 0; c < CH; ++c) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(x[c]) : "l"(m), "l"(k));
+  float s = 0;
+  for (int c = 0; c < CH; ++c) {
+    float a, b;
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x[c]));
+    s += a + b;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 template <typename K>
 void run(const char* name, K k, int elems_per_op, float* out) {
   cudaEvent_t a, b;
@@ -72,7 +103,10 @@ int main() {
     run("f32", k_f32, 1, out);
     run("f16x2", k_f16x2, 2, out);
     run("bf16x2", k_bf16x2, 2, out);
+    run("ffma", k_ffma, 1, out);
+    run("ffma2", k_ffma2, 2, out);
   }
-  printf("(MUFU ex2 at 16 lanes/clk/SM x 148 SMs x 1.9 GHz = %.0f G op/s)\n", 16 * 148 * 1.9);
+  printf("(MUFU ex2 at 16 lanes/clk/SM x 148 SMs x 1.9 GHz = %.0f G op/s; FFMA at 128 = %.0f)\n",
+         16 * 148 * 1.9, 128 * 148 * 1.9);
   return 0;
 }
