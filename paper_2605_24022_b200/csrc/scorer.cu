@@ -407,7 +407,8 @@ struct Fft2Cfg {
   static constexpr size_t ACC_BYTES = (size_t)N * sizeof(double);
   // twiddle tables: f2 [16 r][16 (t&15)], i2 [16 r][R3 (t%R3)], and (when it
   // fits) the per-thread table T3 [16 r][GT t] = W_N^{t r} for f3 / i3
-  static constexpr size_t T2_BYTES = (size_t)16 * (16 + R3) * sizeof(cpx<T>);
+  // (+ 16 entries W_N^{q GT r} for the f3 twiddles of butterflies q > 0)
+  static constexpr size_t T2_BYTES = (size_t)(16 * (16 + R3) + 16) * sizeof(cpx<T>);
   static constexpr size_t T3_BYTES = (size_t)16 * GT * sizeof(cpx<T>);
   static constexpr size_t BASE = SIG_BYTES + TILE_BYTES + ACC_BYTES + T2_BYTES;
   static constexpr bool USE_T3 = BASE + T3_BYTES <= 227 * 1024;
@@ -455,7 +456,8 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
   cpx<T>* t2f = reinterpret_cast<cpx<T>*>(smem_raw + Cfg::SIG_BYTES + Cfg::TILE_BYTES +
                                           Cfg::ACC_BYTES);
   cpx<T>* t2i = t2f + 16 * 16;
-  cpx<T>* t3 = t2i + 16 * R3;
+  cpx<T>* tq = t2i + 16 * R3;  // [Q][R3] W_N^{q GT r}
+  cpx<T>* t3 = tq + 16;
   // tables from the N-point table (exact entries: no products)
   for (int q = threadIdx.x; q < 16 * 16; q += THREADS) {
     const int r = q / 16, u = q % 16;
@@ -466,6 +468,10 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
     cpx<T> w = tw[(u * r * 16) & (N - 1)];
     w.y = -w.y;
     t2i[q] = w;
+  }
+  for (int q = threadIdx.x; q < Q * R3; q += THREADS) {
+    const int qq = q / R3, r = q % R3;
+    tq[q] = tw[(qq * GT * r) & (N - 1)];
   }
   if constexpr (Cfg::USE_T3) {
     for (int q = threadIdx.x; q < 16 * GT; q += THREADS) {
@@ -551,7 +557,7 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
 #pragma unroll
           for (int r = 1; r < R3; ++r) {
             cpx<T> tr = t3[r * GT + t];
-            if (q > 0) tr = cmul(tr, tw[(q * GT * r) & (N - 1)]);
+            if (q > 0) tr = cmul(tr, tq[q * R3 + r]);
             w[r] = cmul(w[r], tr);
           }
         } else {
