@@ -250,6 +250,7 @@ def run_reference(args, rank, world):
 # ---------------------------------------------------------------------------- GPU arm
 
 def run_ours(args, rank, world, local_rank):
+    from paper_2605_24022_b200.distributed import bind_to_gpu_numa
     import torch
     import torch.distributed as dist
     import paper_2605_24022_b200 as ct
@@ -262,6 +263,8 @@ def run_ours(args, rank, world, local_rank):
     c = CONFIGS[args.config]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    # N > 1: each rank on its GPU's NUMA node before the pinned pool is touched
+    numa_cpus = bind_to_gpu_numa(dev.index) if world > 1 else None
     peaks = load_peaks()
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
 
@@ -454,6 +457,7 @@ def run_ours(args, rank, world, local_rank):
         "dtype": "bf16", "data": "synthetic (random-init weights, seeded token ids; chunk KV "
                                  "encoded on the GPU by the same model)",
         "config": {"workload": c["desc"], "parallelism": f"replicas x{world} (request-level)",
+                   "numa_bind": (f"{len(numa_cpus)} GPU-local cpus" if numa_cpus else None),
                    "pool": "importance-ordered, HBM-resident (value) / pinned host (e2e)",
                    "l2": "inputs larger than L2 (4.3 GB pool + 16 GB weights); no flush",
                    "active_rows": eng.A, "n_ctx": eng.n_ctx, "keep_rows_per_chunk": eng.n_keep},
@@ -519,13 +523,16 @@ def run_batch(args, rank, world, local_rank):
     import torch.distributed as dist
     import paper_2605_24022_b200 as ct
     from paper_2605_24022_b200 import _lib
-    from paper_2605_24022_b200.distributed import RequestResult, gather_results, shard_requests
+    from paper_2605_24022_b200.distributed import (RequestResult, bind_to_gpu_numa,
+                                                   gather_results, shard_requests)
     from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
     from paper_2605_24022_b200.pool import KvPool
 
     c = CONFIGS[args.config]
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    # N > 1: each rank on its GPU's NUMA node before the pinned pool is touched
+    numa_cpus = bind_to_gpu_numa(dev.index) if world > 1 else None
     log = (lambda *a: print(*a, file=sys.stderr, flush=True)) if rank == 0 else (lambda *a: None)
     arch = getattr(ct.ModelConfig, c["arch"])
     cfg = arch(n_layers=c["layers"], vocab_size=c["vocab"], seed=1234)
@@ -629,6 +636,7 @@ def run_batch(args, rank, world, local_rank):
         "data": "synthetic (random-init weights, seeded document and suffix token ids; corpus KV "
                 "encoded on the GPU by the same model)",
         "config": {"workload": c["desc"], "parallelism": f"replicas x{world} (request-level)",
+                   "numa_bind": (f"{len(numa_cpus)} GPU-local cpus" if numa_cpus else None),
                    "requests_per_step": n_req, "requests_on_rank0": len(mine),
                    "l2": "inputs larger than L2 (17 GB corpus + 16 GB weights); no flush"},
         "e2e": {"value": n_req * args.steps / (e2e_total * 1e-3), "unit": "requests/s",

@@ -9,6 +9,7 @@ ranks.  The same code runs over gloo on CPU in the tests.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import torch
@@ -80,3 +81,48 @@ def gather_results(local: list[RequestResult], vocab: int, n_selected: int, devi
         if int(out[0][j]) >= 0:
             res.append(RequestResult(int(out[0][j]), float(out[1][j]), out[2][j], out[3][j]))
     return sorted(res, key=lambda r: r.request)
+
+
+def gpu_local_cpus(device_index: int) -> list[int] | None:
+    """Host CPUs on the NUMA node of CUDA device `device_index` (NVML CPU
+    affinity of the device with that PCI bus id), or None when NVML or the
+    device is unavailable."""
+    try:
+        import pynvml
+        props = torch.cuda.get_device_properties(device_index)
+        bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+        pynvml.nvmlInit()
+        try:
+            h = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+            n_words = ((os.cpu_count() or 64) + 63) // 64
+            mask = pynvml.nvmlDeviceGetCpuAffinity(h, n_words)
+        finally:
+            pynvml.nvmlShutdown()
+    except Exception:  # noqa: BLE001 - advisory only
+        return None
+    return cpus_from_mask(mask) or None
+
+
+def cpus_from_mask(mask) -> list[int]:
+    """CPU ids set in an NVML affinity mask (64-bit words, CPU 0 = bit 0 of word 0)."""
+    return [w * 64 + b for w, word in enumerate(mask) for b in range(64) if (int(word) >> b) & 1]
+
+
+def bind_to_gpu_numa(device_index: int) -> list[int] | None:
+    """Pin this rank's process to the CPUs local to its GPU, so the pinned-host
+    chunk pool it allocates next is first-touched on that NUMA node and the
+    per-layer sparse H2D copies never cross the inter-socket link (one process
+    per GPU; eight pools of 3.65 GB/request each at N = 8).  Returns the CPU
+    list, or None (nothing changed) when the affinity cannot be determined."""
+    cpus = gpu_local_cpus(device_index)
+    if not cpus:
+        return None
+    try:
+        allowed = os.sched_getaffinity(0)
+        cpus = [c for c in cpus if c in allowed]
+        if not cpus:
+            return None
+        os.sched_setaffinity(0, cpus)
+    except (AttributeError, OSError):
+        return None
+    return cpus

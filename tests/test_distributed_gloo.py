@@ -68,3 +68,14 @@ def test_gather_and_max_over_two_gloo_ranks():
         assert ttft == 10.0 + i
         assert abs(lsum - float(torch.randn(vocab, generator=g).sum())) < 1e-5
         assert sel == list(range(i, i + 5))
+
+
+def test_numa_mask_decode_and_safe_bind():
+    from paper_2605_24022_b200.distributed import bind_to_gpu_numa, cpus_from_mask
+    assert cpus_from_mask([0b1011, 0]) == [0, 1, 3]
+    assert cpus_from_mask([0, 1 << 63, 1]) == [127, 128]
+    assert cpus_from_mask([]) == []
+    if not torch.cuda.is_available():  # no device: nothing is changed
+        before = os.sched_getaffinity(0)
+        assert bind_to_gpu_numa(0) is None
+        assert os.sched_getaffinity(0) == before
