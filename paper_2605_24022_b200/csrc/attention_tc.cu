@@ -21,6 +21,11 @@
 #include <type_traits>
 #include <cudaTypedefs.h>
 
+// The timing-probe schedules (SCHED 3/4) end the softmax loop body with
+// `continue`, which makes the rest of the body unreachable in those
+// instantiations only.
+#pragma nv_diag_suppress 128
+
 namespace ct {
 
 namespace tc {

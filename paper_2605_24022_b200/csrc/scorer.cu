@@ -420,15 +420,20 @@ struct Fft2Cfg {
 template <typename IN, int N, int TW, int THREADS>
 __device__ __forceinline__ void load_tile(IN* tile, const IN* base, int64_t ld_token, int lt0,
                                           int lane_end, bool vec_ok) {
-  constexpr int CPR = TW * (int)sizeof(IN) / 16;  // 16-B chunks per row
   constexpr bool whole = (TW * sizeof(IN)) % 16 == 0;
-  if (whole && vec_ok && lt0 + TW <= lane_end) {
-    for (int q = threadIdx.x; q < N * CPR; q += THREADS) {
-      const int n = q / CPR, ch = q % CPR;
-      cp_async16(reinterpret_cast<char*>(tile) + (size_t)q * 16,
-                 reinterpret_cast<const char*>(base + (int64_t)n * ld_token + lt0) + ch * 16);
+  if constexpr (whole) {
+    constexpr int CPR = TW * (int)sizeof(IN) / 16;  // 16-B chunks per row
+    if (vec_ok && lt0 + TW <= lane_end) {
+      for (int q = threadIdx.x; q < N * CPR; q += THREADS) {
+        const int n = q / CPR, ch = q % CPR;
+        cp_async16(reinterpret_cast<char*>(tile) + (size_t)q * 16,
+                   reinterpret_cast<const char*>(base + (int64_t)n * ld_token + lt0) + ch * 16);
+      }
+      cp_async_commit();
+      return;
     }
-  } else {
+  }
+  {
     for (int q = threadIdx.x; q < N * TW; q += THREADS) {
       const int n = q / TW, c = q % TW;
       const int lane = lt0 + c;
@@ -444,7 +449,7 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
                    int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff,
                    const cpx<T>* __restrict__ tw, double* __restrict__ partial) {
   using Cfg = Fft2Cfg<T, IN, R3, SPT>;
-  constexpr int N = Cfg::N, GT = Cfg::GT, NS = Cfg::NS, TW = Cfg::TW, THREADS = Cfg::THREADS;
+  constexpr int N = Cfg::N, GT = Cfg::GT, TW = Cfg::TW, THREADS = Cfg::THREADS;
   constexpr int Q = 16 / R3;          // radix-R3 butterflies per thread
   constexpr int NR3 = N / R3;         // = 256
   extern __shared__ __align__(16) unsigned char smem_raw[];

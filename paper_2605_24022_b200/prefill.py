@@ -159,12 +159,26 @@ def _residual_mm(h: torch.Tensor, a: torch.Tensor, w: torch.Tensor) -> None:
         torch.ops.aten.addmm.dtype_out(h, a, w, torch.float32, beta=1, alpha=1, out=h)
 
 
-def run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n_ctx: int,
-               caches: Sequence, reuse: Callable[[int], None] | None = None,
-               record_attention: bool = False, logits_rows: str | None = "all",
-               k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None,
-               timer=None, hook: Callable[[int, str], None] | None = None,
-               record_rows_from: int | None = None, prune_last: bool = True):
+def run_layers(model: GpuModel, *args, **kwargs):
+    """The fp32 mode promises the 1e-5 tolerance: its cuBLAS GEMMs must not
+    silently run as TF32 when a caller enabled that globally, so the flag is
+    cleared for the duration of an fp32 run and restored afterwards."""
+    flags = torch.backends.cuda.matmul
+    if model.dtype != torch.float32 or not flags.allow_tf32:
+        return _run_layers(model, *args, **kwargs)
+    flags.allow_tf32 = False
+    try:
+        return _run_layers(model, *args, **kwargs)
+    finally:
+        flags.allow_tf32 = True
+
+
+def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, n_ctx: int,
+                caches: Sequence, reuse: Callable[[int], None] | None = None,
+                record_attention: bool = False, logits_rows: str | None = "all",
+                k_raw_out: Sequence | None = None, buffers: LayerBuffers | None = None,
+                timer=None, hook: Callable[[int, str], None] | None = None,
+                record_rows_from: int | None = None, prune_last: bool = True):
     """Shared forward engine (ct/toymodel.py:135-193) over device inputs.
 
     tokens/positions: int32 [A] device.  caches[l] = (K, V) [n_ctx, Hkv, D]

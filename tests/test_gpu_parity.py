@@ -418,3 +418,51 @@ def test_llama_geometry_bf16_reduced(ct):
         K, V = res.kv[l]
         assert O.normwise_rel(K.float().cpu().numpy(), want["kv"][l][0]) < BF16_TOL
         assert O.normwise_rel(V.float().cpu().numpy(), want["kv"][l][1]) < BF16_TOL
+
+
+# ---------------------------------------------------------------- Llama geometry, fp32 mode
+
+def test_llama_geometry_fp32_mode_tolerance(ct):
+    """Config-2 geometry (GQA 32/8, D=128, SwiGLU 14336) in the fp32 mode at
+    2 layers / 2 x 1024 chunks / S=32 vs the float64 oracle: selection orders
+    bit-exact, first-token logits and blended K/V within the north star's fp32
+    tolerance (1e-5 normwise).  TF32 is switched on globally for the run to
+    check that the fp32 mode's GEMMs ignore it."""
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=1024, seed=9)
+    gm = ct.GpuModel.random(cfg, dtype=torch.float32)
+    rng = np.random.default_rng(10)
+    toks = [rng.integers(0, 1024, size=1024) for _ in range(2)]
+    suffix = rng.integers(0, 1024, size=32)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = True
+    try:
+        chunks = [ct.encode_chunk_isolated(gm, t, chunk_id=f"f{j}") for j, t in enumerate(toks)]
+        ranks = [ct.rank_chunk(c) for c in chunks]
+        res = ct.selective_prefill(gm, chunks, ranks, suffix, 0.15, logits_rows="last")
+        torch.cuda.synchronize()
+        assert torch.backends.cuda.matmul.allow_tf32  # restored
+    finally:
+        torch.backends.cuda.matmul.allow_tf32 = prev
+    ocfg = O.ModelConfig(seed=9, n_layers=2, n_heads=32, head_dim=128, vocab_size=1024,
+                         mlp="swiglu", n_kv_heads=8, intermediate=14336)
+    om = O.Model(ocfg, weights=gm.to_numpy_weights())
+    # the chunk KV itself is checked against the oracle's isolated encoding
+    for c, t in zip(chunks, toks):
+        kr, vs = O.encode_chunk_isolated(om, t)
+        for l in range(2):
+            assert O.normwise_rel(c.keys[l].cpu().numpy(), kr[l]) < FP32_TOL
+            assert O.normwise_rel(c.values[l].cpu().numpy(), vs[l]) < FP32_TOL
+    och = [([c.keys[l].cpu().numpy() for l in range(2)],
+            [c.values[l].cpu().numpy() for l in range(2)], t) for c, t in zip(chunks, toks)]
+    aggs = [O.rank_chunk(kr, vs)[2] for kr, vs, _ in och]
+    for rk, agg in zip(ranks, aggs):
+        assert np.array_equal(rk.aggregate_order, agg)
+    want = O.selective_prefill(om, och, aggs, suffix, 0.15, want_probs=False,
+                               logits_rows="last")
+    errs = {"logits": O.normwise_rel(res.logits.double().cpu().numpy(), want["logits"])}
+    for l in range(2):
+        K, V = res.kv[l]
+        errs[f"K{l}"] = O.normwise_rel(K.cpu().numpy(), want["kv"][l][0])
+        errs[f"V{l}"] = O.normwise_rel(V.cpu().numpy(), want["kv"][l][1])
+    print("fp32 mode, Llama geometry:", {k: f"{v:.2e}" for k, v in errs.items()})
+    assert max(errs.values()) < FP32_TOL, errs
