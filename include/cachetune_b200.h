@@ -88,6 +88,18 @@ int ct_score_chunks_band(const void* keys, const void* values, int dtype,
                          int32_t* layer_order, int32_t* agg_order,
                          void* workspace, size_t workspace_bytes, void* stream);
 
+/* Single-chunk form of ct_score_chunks (the reference's rank_chunk /
+ * low_freq_scores, ct/spectral.py:82-90,149-159): one chunk of L layers laid
+ * out [L][N][ld_token] with lanes = H*D, exact (f64) mode, cutoff computed
+ * here as floor(alpha * (N/2 + 1)) (ct/spectral.py:57-58).  alpha outside
+ * [0,1] -> CT_ERR_PARAM before any work.  layer_scores [L][N] f64,
+ * agg_scores [N] f64, agg_order [N] int32 (stable descending). */
+int ct_score_chunk(const void* keys, const void* values, int dtype,
+                   int64_t L, int64_t N, int64_t H, int64_t D, int64_t ld_token,
+                   double alpha, double* layer_scores, double* agg_scores,
+                   int32_t* agg_order, void* workspace, size_t workspace_bytes,
+                   void* stream);
+
 /* Stable descending argsort of `rows` rows of n f64 scores (ties -> lower
  * index): ct/spectral.py:99-101.  order is int32 [rows][n]. */
 int ct_desc_order(const double* scores, int64_t rows, int64_t n,
@@ -102,6 +114,14 @@ int ct_desc_order(const double* scores, int64_t rows, int64_t n,
  * [sum (N_j-k_j)], keep_src_row [sum(N_j-k_j)] = importance rank of each keep
  * token (its row in an importance-ordered pool).  offsets/ks/rec_base/
  * keep_base are DEVICE int64 arrays of n_chunks(+1) entries. */
+/* One chunk's selection at ratio r -- selection_count / indices_for_ratio /
+ * complement_for_ratio (ct/spectral.py:162-184): k = min(max(ceil(r*n -
+ * 1e-9), 0), n) computed on the host (written to *k_out when non-NULL);
+ * sel [k] = order[0..k) ascending, keep [n-k] = order[k..n) ascending (device
+ * int32, chunk-local ids).  r outside [0,1] -> CT_ERR_PARAM before any work. */
+int ct_select(const int32_t* order, int64_t n, double r, int32_t* sel,
+              int32_t* keep, int64_t* k_out, void* stream);
+
 int ct_selection_plan(const int32_t* agg_orders, const int64_t* offsets,
                       const int64_t* ks, const int64_t* rec_base,
                       const int64_t* keep_base, int64_t n_chunks,

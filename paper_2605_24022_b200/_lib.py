@@ -62,6 +62,10 @@ _SIGS = {
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                      c_void_p]),
     "ct_desc_order": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "ct_score_chunk": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
+                               c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                               c_size_t, c_void_p]),
+    "ct_select": (c_int, [c_void_p, c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ct_selection_plan": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_int64,
                                   c_int64, c_void_p, c_void_p, c_void_p, c_void_p]),
     "ct_rope_table": (c_int, [c_void_p, c_int64, c_int64, c_double, c_void_p, c_void_p,

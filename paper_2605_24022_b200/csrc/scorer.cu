@@ -998,24 +998,17 @@ desc_order_kernel(const double* __restrict__ scores, int n, int P, int32_t* __re
 // aggregate order, then emits recomputed / kept tokens in ascending order
 // (ct/spectral.py:175-184) on the global axis (offset by the chunk start).
 constexpr int PLAN_THREADS = 1024;
-__global__ void __launch_bounds__(PLAN_THREADS)
-selection_plan_kernel(const int32_t* __restrict__ agg_orders, const int64_t* __restrict__ offsets,
-                      const int64_t* __restrict__ ks, const int64_t* __restrict__ rec_base,
-                      const int64_t* __restrict__ keep_base, int32_t* __restrict__ rec_global,
-                      int32_t* __restrict__ keep_global, int32_t* __restrict__ keep_src_row) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int c = blockIdx.x;
-  const int64_t off = offsets[c];
-  const int n = (int)(offsets[c + 1] - off);
-  const int k = (int)ks[c];
-  int* rank = reinterpret_cast<int*>(smem_raw);  // importance rank of each token
-  __shared__ int warp_tot[PLAN_THREADS / 32];
-  const int32_t* agg = agg_orders + off;
+// One chunk's plan: tokens [off, off + n) with aggregate order agg[0..n); the
+// first k ranks are recomputed.  rec / keep ascending, ksrc = rank of each
+// keep token (nullable).  rank[] = n ints of shared memory.
+__device__ __forceinline__ void plan_one(const int32_t* __restrict__ agg, int64_t off, int n,
+                                         int k, int* rank, int* warp_tot, int32_t* rec,
+                                         int32_t* keep, int32_t* ksrc) {
   for (int i = threadIdx.x; i < n; i += PLAN_THREADS) rank[agg[i]] = i;
   __syncthreads();
   // contiguous segment per thread
   const int per = (n + PLAN_THREADS - 1) / PLAN_THREADS;
-  const int t0 = threadIdx.x * per, t1 = min(n, t0 + per);
+  const int t0 = min(n, (int)threadIdx.x * per), t1 = min(n, t0 + per);
   int cnt = 0;
   for (int t = t0; t < t1; ++t) cnt += rank[t] < k;
   // block exclusive scan of cnt
@@ -1028,20 +1021,17 @@ selection_plan_kernel(const int32_t* __restrict__ agg_orders, const int64_t* __r
   if (lane == 31) warp_tot[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    int w = warp_tot[lane];
+    int w = lane < PLAN_THREADS / 32 ? warp_tot[lane] : 0;
     int wi = w;
     for (int d = 1; d < 32; d <<= 1) {
       int v = __shfl_up_sync(0xffffffffu, wi, d);
       if (lane >= d) wi += v;
     }
-    warp_tot[lane] = wi - w;
+    if (lane < PLAN_THREADS / 32) warp_tot[lane] = wi - w;
   }
   __syncthreads();
   int rpos = warp_tot[warp] + incl - cnt;  // recomputed tokens before my segment
   int kpos = t0 - rpos;                    // kept tokens before my segment
-  int32_t* rec = rec_global + rec_base[c];
-  int32_t* keep = keep_global + keep_base[c];
-  int32_t* ksrc = keep_src_row ? keep_src_row + keep_base[c] : nullptr;
   for (int t = t0; t < t1; ++t) {
     const int rk = rank[t];
     if (rk < k) {
@@ -1051,6 +1041,29 @@ selection_plan_kernel(const int32_t* __restrict__ agg_orders, const int64_t* __r
       keep[kpos++] = (int32_t)(off + t);
     }
   }
+}
+
+__global__ void __launch_bounds__(PLAN_THREADS)
+selection_plan_kernel(const int32_t* __restrict__ agg_orders, const int64_t* __restrict__ offsets,
+                      const int64_t* __restrict__ ks, const int64_t* __restrict__ rec_base,
+                      const int64_t* __restrict__ keep_base, int32_t* __restrict__ rec_global,
+                      int32_t* __restrict__ keep_global, int32_t* __restrict__ keep_src_row) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tot[PLAN_THREADS / 32];
+  const int c = blockIdx.x;
+  const int64_t off = offsets[c];
+  plan_one(agg_orders + off, off, (int)(offsets[c + 1] - off), (int)ks[c],
+           reinterpret_cast<int*>(smem_raw), warp_tot, rec_global + rec_base[c],
+           keep_global + keep_base[c], keep_src_row ? keep_src_row + keep_base[c] : nullptr);
+}
+
+// ct_select: one chunk, scalar k (chunk-local token ids)
+__global__ void __launch_bounds__(PLAN_THREADS)
+select_kernel(const int32_t* __restrict__ order, int n, int k, int32_t* __restrict__ sel,
+              int32_t* __restrict__ keep) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int warp_tot[PLAN_THREADS / 32];
+  plan_one(order, 0, n, k, reinterpret_cast<int*>(smem_raw), warp_tot, sel, keep, nullptr);
 }
 
 static int ilog2_exact(int64_t n) {
@@ -1283,4 +1296,38 @@ extern "C" int ct_selection_plan(const int32_t* agg_orders, const int64_t* offse
   selection_plan_kernel<<<(unsigned)n_chunks, PLAN_THREADS, smem, (cudaStream_t)stream>>>(
       agg_orders, offsets, ks, rec_base, keep_base, rec_global, keep_global, keep_src_row);
   return check_launch("selection_plan_kernel");
+}
+
+// ct/spectral.py:162-184 for one chunk: k = min(max(ceil(r N - 1e-9), 0), N)
+// (the reference's float guard, same double arithmetic); the first k entries
+// of `order` ascending -> sel [k], the rest ascending -> keep [N - k].
+extern "C" int ct_select(const int32_t* order, int64_t n, double r, int32_t* sel, int32_t* keep,
+                         int64_t* k_out, void* stream) {
+  if (!(r >= 0.0 && r <= 1.0)) return fail(CT_ERR_PARAM, "ratio must be in [0, 1], got %g", r);
+  if (n < 0) return fail(CT_ERR_SHAPE, "negative token count %lld", (long long)n);
+  int64_t k = (int64_t)ceil(r * (double)n - 1e-9);
+  k = k < 0 ? 0 : (k > n ? n : k);
+  if (k_out) *k_out = k;
+  if (n == 0) return CT_OK;
+  const size_t smem = (size_t)n * sizeof(int);
+  if (smem > 200 * 1024) return fail(CT_ERR_UNSUPPORTED, "chunk of %lld tokens", (long long)n);
+  CT_CUDA(cudaFuncSetAttribute(select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem));
+  select_kernel<<<1, PLAN_THREADS, smem, (cudaStream_t)stream>>>(order, (int)n, (int)k, sel, keep);
+  return check_launch("select_kernel");
+}
+
+// One chunk of L layers [L][N][ld_token] (lanes = H*D), exact (f64) mode, with
+// the reference's cutoff floor(alpha * (N/2 + 1)) (ct/spectral.py:57-58,82-90).
+extern "C" int ct_score_chunk(const void* keys, const void* values, int dtype, int64_t L,
+                              int64_t N, int64_t H, int64_t D, int64_t ld_token, double alpha,
+                              double* layer_scores, double* agg_scores, int32_t* agg_order,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  if (!(alpha >= 0.0 && alpha <= 1.0))
+    return fail(CT_ERR_PARAM, "alpha must be in [0, 1], got %g", alpha);
+  if (H < 1 || D < 1) return fail(CT_ERR_SHAPE, "H=%lld D=%lld", (long long)H, (long long)D);
+  const int64_t cutoff = (int64_t)floor(alpha * (double)(N / 2 + 1));
+  return ct_score_chunks(keys, values, dtype, 1, L, N, H * D, ld_token, N * ld_token,
+                         L * N * ld_token, cutoff, CT_F64, layer_scores, agg_scores, nullptr,
+                         agg_order, workspace, workspace_bytes, stream);
 }

@@ -10,6 +10,8 @@ reference's pocketfft so per-layer and aggregate orders are bit-exact;
 
 from __future__ import annotations
 
+import ctypes
+
 import math
 from dataclasses import dataclass
 
@@ -246,21 +248,32 @@ def select_device(agg_orders: list, ratios, device=None):
     return rec, keep, ksrc, ks
 
 
-def indices_for_ratio(ranking, r: float) -> np.ndarray:
-    """First ceil(r*N) tokens of the aggregate order, ascending (ct/spectral.py:175-178)."""
-    selection_count(r, ranking.n_tokens)  # validates r
+def _select_one(ranking, r: float):
+    """ct_select on one ranking: (selected ascending, kept ascending) int32 on
+    the device, k computed by the C ABI with the reference's guard."""
+    n = int(ranking.n_tokens)
+    k = selection_count(r, n)  # validates r (InvalidParam before any work)
     dev = _dev.require_cuda()
     agg = (ranking.aggregate_device(dev) if isinstance(ranking, ImportanceRanking)
            else torch.as_tensor(np.asarray(ranking.aggregate_order, np.int32), device=dev))
-    rec, _, _, _ = select_device([agg], r, dev)
-    return rec.cpu().numpy().astype(np.int64)
+    agg = agg.to(torch.int32).contiguous()
+    sel = torch.empty(k, dtype=torch.int32, device=dev)
+    keep = torch.empty(n - k, dtype=torch.int32, device=dev)
+    k_abi = ctypes.c_int64(-1)
+    _lib.call("ct_select", _dev.ptr(agg), n, float(r), _dev.ptr(sel), _dev.ptr(keep),
+              ctypes.addressof(k_abi), _dev.stream_handle())
+    if k_abi.value != k:  # pragma: no cover - the two restatements must agree
+        raise RuntimeError(f"ct_select k={k_abi.value}, selection_count={k}")
+    return sel, keep
+
+
+def indices_for_ratio(ranking, r: float) -> np.ndarray:
+    """First ceil(r*N) tokens of the aggregate order, ascending (ct/spectral.py:175-178)."""
+    sel, _ = _select_one(ranking, r)
+    return sel.cpu().numpy().astype(np.int64)
 
 
 def complement_for_ratio(ranking, r: float) -> np.ndarray:
     """Tokens NOT selected at ratio r, ascending (ct/spectral.py:181-184)."""
-    selection_count(r, ranking.n_tokens)
-    dev = _dev.require_cuda()
-    agg = (ranking.aggregate_device(dev) if isinstance(ranking, ImportanceRanking)
-           else torch.as_tensor(np.asarray(ranking.aggregate_order, np.int32), device=dev))
-    _, keep, _, _ = select_device([agg], r, dev)
+    _, keep = _select_one(ranking, r)
     return keep.cpu().numpy().astype(np.int64)

@@ -26,7 +26,9 @@ def lib():
 
 def test_header_declares_entry_points():
     syms = header_symbols()
-    for want in ("ct_score_chunks", "ct_selection_plan", "ct_gather_rope_blend",
+    # SURVEY.md section 8(b) minimum exports (+ the batched / plan forms)
+    for want in ("ct_score_chunk", "ct_select", "ct_score_chunks", "ct_selection_plan",
+                 "ct_gather_rope_blend",
                  "ct_qkv_rope_scatter", "ct_selective_attention", "ct_copy_ranges_h2d"):
         assert want in syms
 
@@ -49,6 +51,23 @@ def test_version_and_error_plumbing(lib):
     assert st == 1
     with pytest.raises(_lib.ShapeError):
         _lib.check(st, "ct_desc_order")
+
+
+def test_select_and_score_chunk_validate_before_work(lib):
+    from paper_2605_24022_b200 import _lib
+    nan = float("nan")
+    for r in (-0.01, 1.5, nan):  # ct/spectral.py:169-170 -> InvalidParam, no launch
+        assert lib.ct_select(None, 16, r, None, None, None, None) == 2
+    with pytest.raises(_lib.InvalidParam):
+        _lib.check(lib.ct_select(None, 16, 2.0, None, None, None, None), "ct_select")
+    for a in (-0.5, 1.01, nan):  # ct/spectral.py:39-40
+        assert lib.ct_score_chunk(None, None, 0, 1, 8, 1, 1, 1, a, None, None, None,
+                                  None, 0, None) == 2
+    # empty chunk: k = 0, nothing launched
+    import ctypes
+    k = ctypes.c_int64(-1)
+    assert lib.ct_select(None, 0, 0.5, None, None, ctypes.addressof(k), None) == 0
+    assert k.value == 0
 
 
 def test_workspace_query_is_host_only(lib):

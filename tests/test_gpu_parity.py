@@ -51,6 +51,47 @@ def test_spectral_cases_bit_exact(ct):
             assert np.array_equal(ct.indices_for_ratio(rk, r), g[f"c{i}_{tag}"]), (i, r)
 
 
+def test_c_abi_score_chunk_and_select_minimum_exports(ct):
+    """The single-chunk C entry points (SURVEY 8(b) minimum exports) on the
+    golden spectral cases: ct_score_chunk scores/orders == the reference's
+    rank_chunk, ct_select == indices_for_ratio / complement_for_ratio,
+    including r = 0, r = 1 and the decimal-ratio guard (0.1 * N)."""
+    import ctypes
+    from paper_2605_24022_b200 import _lib
+    lib = _lib.load()
+    g = golden("spectral_cases")
+    dev = torch.device("cuda")
+    for i in range(int(g["count"])):
+        keys, vals, alpha = g[f"c{i}_keys"], g[f"c{i}_vals"], float(g[f"c{i}_alpha"])
+        L, (N, H, D) = len(keys), keys[0].shape
+        kt = torch.as_tensor(np.stack(keys).astype(np.float32), device=dev).contiguous()
+        vt = torch.as_tensor(np.stack(vals).astype(np.float32), device=dev).contiguous()
+        ws_bytes = lib.ct_score_workspace_bytes(1, L, N, H * D, _lib.CT_F64)
+        ws = torch.empty(max(ws_bytes, 1), dtype=torch.uint8, device=dev)
+        ls = torch.empty((L, N), dtype=torch.float64, device=dev)
+        agg = torch.empty(N, dtype=torch.float64, device=dev)
+        order = torch.empty(N, dtype=torch.int32, device=dev)
+        _lib.call("ct_score_chunk", kt.data_ptr(), vt.data_ptr(), _lib.CT_F32, L, N, H, D, H * D,
+                  alpha, ls.data_ptr(), agg.data_ptr(), order.data_ptr(), ws.data_ptr(),
+                  ws_bytes, None)
+        torch.cuda.synchronize()
+        want = g[f"c{i}_scores"]
+        np.testing.assert_allclose(ls.cpu().numpy(), want, rtol=1e-11,
+                                   atol=1e-13 * max(1.0, float(np.max(want))), err_msg=str(i))
+        assert np.array_equal(order.cpu().numpy(), g[f"c{i}_agg"]), i
+        for r in (0.0, 0.05, 0.1, 0.15, 0.5, 1.0):
+            k = ctypes.c_int64(-1)
+            kk = O.selection_count(r, N)
+            sel = torch.empty(kk, dtype=torch.int32, device=dev)
+            keep = torch.empty(N - kk, dtype=torch.int32, device=dev)
+            _lib.call("ct_select", order.data_ptr(), N, r, sel.data_ptr(), keep.data_ptr(),
+                      ctypes.addressof(k), None)
+            torch.cuda.synchronize()
+            assert k.value == kk, (i, r)
+            assert np.array_equal(sel.cpu().numpy(), O.indices_for_ratio(g[f"c{i}_agg"], r))
+            assert np.array_equal(keep.cpu().numpy(), O.complement_for_ratio(g[f"c{i}_agg"], r))
+
+
 def test_highband_cases_bit_exact(ct):
     """Device high band (ct_score_chunks_band, band=1) vs the reference's
     highfreq strategy ranking (ct/toymodel.py:356-363)."""
