@@ -507,3 +507,25 @@ def test_llama_geometry_fp32_mode_tolerance(ct):
         errs[f"V{l}"] = O.normwise_rel(V.cpu().numpy(), want["kv"][l][1])
     print("fp32 mode, Llama geometry:", {k: f"{v:.2e}" for k, v in errs.items()})
     assert max(errs.values()) < FP32_TOL, errs
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 1023, 1025, 2048, 4097, 50000])
+def test_c_abi_select_random_orders(ct, n):
+    """ct_select on random permutations (single-CTA plan up to 50K tokens)
+    vs the oracle's integer rules at random and boundary ratios."""
+    import ctypes
+    from paper_2605_24022_b200 import _lib
+    rng = np.random.default_rng(n)
+    order = rng.permutation(n).astype(np.int32)
+    od = torch.as_tensor(order, device="cuda")
+    for r in (0.0, 1.0, 0.15, 0.1, *rng.random(4).tolist()):
+        kk = O.selection_count(r, n)
+        sel = torch.empty(kk, dtype=torch.int32, device="cuda")
+        keep = torch.empty(n - kk, dtype=torch.int32, device="cuda")
+        k = ctypes.c_int64(-1)
+        _lib.call("ct_select", od.data_ptr(), n, r, sel.data_ptr(), keep.data_ptr(),
+                  ctypes.addressof(k), None)
+        torch.cuda.synchronize()
+        assert k.value == kk
+        assert np.array_equal(sel.cpu().numpy(), O.indices_for_ratio(order, r))
+        assert np.array_equal(keep.cpu().numpy(), O.complement_for_ratio(order, r))
