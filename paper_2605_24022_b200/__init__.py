@@ -30,6 +30,8 @@ _LAZY = {
     "effective_ratio": "experiments", "run_selection_experiment": "experiments",
     "FrequencyTokenRanker": "estimators", "RatioCalibrator": "estimators",
     # serving surface: resident pool + preallocated per-request engine
+    "CachePool": "cachepool", "token_row_bytes": "cachepool", "TierConfig": "pipesim",
+    "TIER_PRESETS": "pipesim", "write_ctkv": "ctkv", "read_ctkv": "ctkv",
     "KvPool": "pool", "SelectivePrefillEngine": "pipeline", "FullPrefillEngine": "pipeline",
     "prepare_pool": "offline", "calibrate": "scheduler", "SearchConfig": "scheduler",
     "HardwareProfile": "scheduler",

@@ -148,3 +148,53 @@ def test_offline_prepare_pool_and_ctkv_export(ct, tmp_path):
         # the exported chunk KV is the oracle's isolated encoding (fp32 mode)
         kr, vs = O.encode_chunk_isolated(om, toks[i])
         assert O.normwise_rel(chunk.keys_raw[1].data, kr[1]) < 1e-5
+
+
+@pytest.mark.parametrize("file_backed", [False, True])
+def test_cachepool_fetch_sparse_bit_exact_into_hbm(ct, tmp_path, file_backed):
+    """CachePool.fetch_sparse (ct/cachepool.py:437-481): exactly the planned
+    byte ranges (the reference's, pinned in tests/test_cachepool.py) staged in
+    pinned memory and moved to HBM in one copy; rows bit-identical to the
+    chunk's K/V at the keep indices, bytes read == expected_bytes; the
+    registry converts to the engine's importance-ordered KvPool."""
+    from oracle import cachetune_oracle as O
+    from paper_2605_24022_b200.cachepool import CachePool
+    from paper_2605_24022_b200.pipesim import TierConfig
+    g = golden("pool_cases")
+    tier = TierConfig("ssd" if file_backed else "cpu-mem", read_bw=535e6, write_bw=445e6,
+                      backing=str(tmp_path) if file_backed else None)
+    pool = CachePool()
+    for i in range(int(g["count"])):
+        l, n, h, d, layer = (int(x) for x in g[f"p{i}_geom"])
+        keys, vals = g[f"p{i}_keys"], g[f"p{i}_vals"]
+        chunk = ct.KvChunk(f"p{i}", tuple(ct.SeqTensor(k) for k in keys),
+                           tuple(ct.SeqTensor(v) for v in vals))
+        scores, orders, agg = O.rank_chunk(list(keys), list(vals))
+        rk = ct.ImportanceRanking(per_layer_scores=scores, per_layer_order=orders,
+                                  aggregate_order=agg, alpha=0.5, n_tokens=n)
+        pool.put_chunk(chunk, rk, tier)
+        for r in (0.0, float(g[f"p{i}_r"]), 0.5, 1.0):
+            plan = pool.plan_sparse_fetch(f"p{i}", layer, r)
+            before = pool.io_stats["bytes_read"]
+            K, V, keep = pool.fetch_sparse(plan)
+            assert pool.io_stats["bytes_read"] - before == plan.expected_bytes
+            if keep.size == 0:
+                assert K is None and V is None
+                continue
+            assert K.is_cuda and K.dtype == torch.float32
+            assert np.array_equal(K.cpu().numpy(), keys[layer][keep])
+            assert np.array_equal(V.cpu().numpy(), vals[layer][keep])
+    # same-geometry chunks -> the engine's importance-ordered pool (f32, HBM)
+    ids = [f"p{i}" for i in range(int(g["count"]))]
+    geo = {pool.geometry(c) for c in ids}
+    c0 = ids[0]
+    same = [c for c in ids if pool.geometry(c) == pool.geometry(c0)]
+    kvp = pool.to_kv_pool(same, "hbm", dtype=torch.float32)
+    for c in same:
+        for r in (0.15, 0.5):
+            a = pool.fetch_sparse(pool.plan_sparse_fetch(c, 0, r))
+            b = kvp.fetch_sparse(kvp.plan_sparse_fetch(c, 0, r))
+            assert np.array_equal(a[2], b[2])
+            if a[2].size:
+                assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+    assert len(geo) >= 1
