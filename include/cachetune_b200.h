@@ -143,7 +143,8 @@ int ct_rope_table(const double* freqs, int64_t half_dim, int64_t n_pos,
 
 /* Rotate rows: out[i] = rope(x[i], positions[i]) (ct/rope.py:75-81).
  * x/out [n][H][D] of dtype; f32/bf16 in; math in f64 for CT_F32 (bit-exact
- * formula of ct/rope.py:61-62), f32 for CT_BF16. */
+ * formula of ct/rope.py:61-62), f32 for CT_BF16; CT_F64 rows in and out are
+ * ct/rope.py:47-72 rope_rotate (f64 table required). */
 int ct_rope_apply(const void* x, const int32_t* positions, int64_t n,
                   int64_t H, int64_t D, int dtype, int pairing,
                   const void* table, void* out, void* stream);

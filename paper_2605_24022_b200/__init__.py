@@ -19,10 +19,12 @@ _LAZY = {
     "low_freq_scores": "spectral", "high_freq_scores": "spectral",
     "indices_for_ratio": "spectral",
     "complement_for_ratio": "spectral", "selection_count": "spectral",
-    "cutoff_index": "spectral", "score_device": "spectral", "select_device": "spectral",
-    "RopeParams": "rope", "rope_apply": "rope",
+    "cutoff_index": "spectral", "rfft_seq": "spectral", "irfft_seq": "spectral",
+    "lowpass": "spectral", "highpass": "spectral", "jaccard_overlap": "spectral",
+    "selection_stability": "spectral", "ComplexSpectrum": "kvcore", "score_device": "spectral", "select_device": "spectral",
+    "RopeParams": "rope", "rope_apply": "rope", "rope_rotate": "rope",
     "fuse_layer": "blend", "tensor_scatter_tokens": "blend",
-    "ModelConfig": "model", "GpuModel": "model",
+    "ModelConfig": "model", "GpuModel": "model", "ToyModel": "model", "ToyModelConfig": "model",
     "selective_prefill": "prefill", "full_prefill": "prefill",
     "encode_chunk_isolated": "prefill", "PrefillResult": "prefill",
     "AttentionRecord": "prefill", "attention_deviation": "prefill",

@@ -25,7 +25,7 @@ def _to_dev(t, dev):
     if isinstance(t, torch.Tensor):
         return t.to(dev).contiguous()
     data = t.data if hasattr(t, "data") and not isinstance(t, np.ndarray) else t
-    return torch.from_numpy(np.ascontiguousarray(np.asarray(data, dtype=np.float32))).to(dev)
+    return torch.from_numpy(np.require(data, np.float32, ["C", "W"])).to(dev)
 
 
 def scatter_rows_device(dst: torch.Tensor, src: torch.Tensor, idx: torch.Tensor) -> None:

@@ -419,14 +419,44 @@ extern "C" int ct_rope_table(const double* freqs, int64_t half_dim, int64_t n_po
   return check_launch("rope_table_kernel");
 }
 
+// f64 rows in and out (ct/rope.py:47-72 rope_rotate, which returns float64):
+// ra = a cos - b sin, rb = a sin + b cos as separate correctly rounded
+// products and sums (no FMA contraction), like numpy's elementwise ops.
+__global__ void __launch_bounds__(256)
+rope_rotate_f64_kernel(const double* __restrict__ x, const int32_t* __restrict__ positions,
+                       int64_t n, int H, int D, int pairing, const double2* __restrict__ table,
+                       double* __restrict__ out) {
+  const int half = D / 2;
+  const int64_t total = n * H * half;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < total;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = u / (H * half);
+    const int rem = (int)(u % (H * half));
+    const int h = rem / half, j = rem % half;
+    const double2 cs = __ldg(table + (int64_t)positions[row] * half + j);
+    const int ia = pairing == CT_ROPE_ADJACENT ? 2 * j : j;
+    const int ib = pairing == CT_ROPE_ADJACENT ? 2 * j + 1 : j + half;
+    const int64_t base = (row * H + h) * (int64_t)D;
+    const double a = x[base + ia], b = x[base + ib];
+    out[base + ia] = __dsub_rn(__dmul_rn(a, cs.x), __dmul_rn(b, cs.y));
+    out[base + ib] = __dadd_rn(__dmul_rn(a, cs.y), __dmul_rn(b, cs.x));
+  }
+}
+
 extern "C" int ct_rope_apply(const void* x, const int32_t* positions, int64_t n, int64_t H,
                              int64_t D, int dtype, int pairing, const void* table, void* out,
                              void* stream) {
   if (D < 2 || D % 2) return fail(CT_ERR_SHAPE, "head_dim must be even, got %lld", (long long)D);
-  if (!valid_dtype(dtype)) return fail(CT_ERR_PARAM, "dtype %d", dtype);
+  if (!valid_dtype(dtype) && dtype != CT_F64) return fail(CT_ERR_PARAM, "dtype %d", dtype);
   if (pairing != CT_ROPE_ADJACENT && pairing != CT_ROPE_SPLIT) return fail(CT_ERR_PARAM, "pairing");
   if (n == 0) return CT_OK;
   cudaStream_t st = (cudaStream_t)stream;
+  if (dtype == CT_F64) {
+    rope_rotate_f64_kernel<<<grid_for(n * H * (D / 2), 256), 256, 0, st>>>(
+        (const double*)x, positions, n, (int)H, (int)D, pairing, (const double2*)table,
+        (double*)out);
+    return check_launch("rope_rotate_f64_kernel");
+  }
   const bool f64m = dtype == CT_F32;
   const bool v4 = (D / 2) % 4 == 0;
   const int64_t units = n * H * (D / 2) / (v4 ? 4 : 1);

@@ -97,7 +97,7 @@ class GpuModel:
     def from_numpy(cls, config: ModelConfig, embedding, layers, w_out,
                    dtype=torch.float32, device="cuda"):
         def up(a):
-            return torch.from_numpy(np.ascontiguousarray(np.asarray(a, dtype=np.float64))) \
+            return torch.from_numpy(np.require(a, np.float64, ["C", "W"])) \
                 .to(device=device, dtype=dtype)
         glayers = []
         for layer in layers:
@@ -193,3 +193,15 @@ class GpuModel:
             layers.append(layer)
         return {"embedding": self.embedding.double().cpu().numpy(), "layers": layers,
                 "w_out": self.w_out.double().cpu().numpy()}
+
+
+# Drop-in names of ct/toymodel.py:31-85: the reference's config fields are a
+# subset of ModelConfig's (same names and defaults), and a ToyModel is the
+# seeded reference geometry with its weights resident in HBM.
+ToyModelConfig = ModelConfig
+
+
+def ToyModel(config: ModelConfig, dtype=torch.float32, device="cuda") -> GpuModel:  # noqa: N802
+    """The reference ToyModel (ct/toymodel.py:58-79) on the device: same seed ->
+    same weights (GpuModel.reference_init), fp32 by default (the 1e-5 mode)."""
+    return GpuModel.reference_init(config, dtype=dtype, device=device)

@@ -102,7 +102,7 @@ def rope_apply_device(x: torch.Tensor, positions: torch.Tensor, params) -> torch
     out = torch.empty_like(x)
     if n == 0:
         return out
-    kind = "f64" if x.dtype == torch.float32 else "f32"
+    kind = "f64" if x.dtype in (torch.float32, torch.float64) else "f32"
     tab = rope_table_for(params, positions, kind)
     rows = torch.arange(n, dtype=torch.int32, device=x.device)
     _lib.call("ct_rope_apply", _dev.ptr(x), _dev.ptr(rows), n, h, d,
@@ -121,6 +121,29 @@ def rope_apply(keys, positions: Sequence[int], params) -> SeqTensor:
     if data.shape[2] != params.head_dim:
         raise ShapeError(f"tensor head_dim {data.shape[2]} != params head_dim {params.head_dim}")
     dev = _dev.require_cuda()
-    x = torch.from_numpy(np.ascontiguousarray(data)).to(dev)
+    x = torch.from_numpy(np.require(data, None, ["C", "W"])).to(dev)
     p = torch.as_tensor(pos.astype(np.int64), device=dev)
     return SeqTensor(rope_apply_device(x, p, params).cpu().numpy())
+
+
+def rope_rotate(x, positions, params):
+    """ct/rope.py:47-72: rotate an [N, H, D] array at `positions` in float64
+    arithmetic and return float64 (numpy in -> numpy out, torch -> torch on
+    the device).  ct_rope_apply with f64 rows: unfused products and sums, so
+    the result equals numpy's up to the cos/sin of the angle table (<= 1 ulp)."""
+    params = as_rope_params(params)
+    as_numpy = not isinstance(x, torch.Tensor)
+    shape = tuple(np.shape(x))
+    if len(shape) != 3:
+        raise ShapeError(f"expected [N, H, D], got shape {shape}")
+    if shape[2] != params.head_dim:
+        raise ShapeError(f"tensor head_dim {shape[2]} != params head_dim {params.head_dim}")
+    dev = _dev.require_cuda() if as_numpy else x.device
+    xt = (torch.from_numpy(np.require(x, np.float64, ["C", "W"])).to(dev) if as_numpy
+          else x.to(torch.float64))
+    pos = torch.as_tensor(np.asarray(positions, dtype=np.int64) if as_numpy
+                          else positions, device=dev).to(torch.int64)
+    if pos.numel() != shape[0]:
+        raise ShapeError(f"{pos.numel()} positions for {shape[0]} tokens")
+    out = rope_apply_device(xt, pos, params)
+    return out.cpu().numpy() if as_numpy else out

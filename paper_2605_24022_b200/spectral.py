@@ -20,7 +20,7 @@ import torch
 
 from . import _dev, _lib
 from .errors import InvalidParam, ShapeError
-from .kvcore import DeviceChunk, KvChunk, SeqTensor
+from .kvcore import ComplexSpectrum, DeviceChunk, KvChunk, SeqTensor
 
 DEFAULT_ALPHA = 0.5  # ct/spectral.py:24
 
@@ -277,3 +277,73 @@ def complement_for_ratio(ranking, r: float) -> np.ndarray:
     """Tokens NOT selected at ratio r, ascending (ct/spectral.py:181-184)."""
     _, keep = _select_one(ranking, r)
     return keep.cpu().numpy().astype(np.int64)
+
+
+# -- spectrum building blocks (ct/spectral.py:27-66) and selection diagnostics
+# (:187-208).  Analysis helpers, NOT the scoring path: low_freq_scores /
+# rank_chunk run the fused FFT -> band mask -> inverse FFT -> energy kernel
+# and never materialise a spectrum.  The transforms here are cuFFT (torch.fft)
+# in float64 on the device, the same role spectrum_report gives them.
+
+def _seq_device(t) -> torch.Tensor:
+    if isinstance(t, torch.Tensor):
+        return t.to(torch.float64)
+    data = np.asarray(t.data if hasattr(t, "data") else t, dtype=np.float64)
+    if data.ndim != 3:
+        raise ShapeError(f"expected [token][head][dim], got ndim={data.ndim}")
+    return torch.from_numpy(np.require(data, None, ["C", "W"])).to(_dev.require_cuda())
+
+
+def rfft_seq(t) -> ComplexSpectrum:
+    """Real FFT along the token axis of every (head, dim) lane (ct/spectral.py:27-34)."""
+    x = _seq_device(t)
+    spec = torch.fft.rfft(x, dim=0).cpu().numpy()
+    return ComplexSpectrum.from_complex(spec, origin_len=int(x.shape[0]))
+
+
+def lowpass(s: ComplexSpectrum, alpha: float) -> ComplexSpectrum:
+    """Zero every bin at index >= floor(alpha * n_freqs) (ct/spectral.py:37-44)."""
+    _check_alpha(alpha)
+    c = cutoff_index(alpha, s.n_freqs)
+    kept = s.to_complex()
+    kept[c:] = 0.0
+    return ComplexSpectrum.from_complex(kept, origin_len=s.origin_len)
+
+
+def highpass(s: ComplexSpectrum, alpha: float) -> ComplexSpectrum:
+    """Zero the bins below the same cutoff (ct/spectral.py:47-54)."""
+    _check_alpha(alpha)
+    c = cutoff_index(alpha, s.n_freqs)
+    kept = s.to_complex()
+    kept[:c] = 0.0
+    return ComplexSpectrum.from_complex(kept, origin_len=s.origin_len)
+
+
+def irfft_seq(s: ComplexSpectrum, n: int) -> SeqTensor:
+    """Inverse of rfft_seq back to n real tokens, f32 (ct/spectral.py:61-66)."""
+    if n != s.origin_len:
+        raise ShapeError(f"requested length {n} != origin_len {s.origin_len}")
+    spec = torch.from_numpy(np.require(s.to_complex(), None, ["C", "W"])).to(_dev.require_cuda())
+    real = torch.fft.irfft(spec, n=n, dim=0).cpu().numpy()
+    return SeqTensor(real.astype(np.float32))
+
+
+def jaccard_overlap(a, b) -> float:
+    """|a & b| / |a | b| of two index sets; 1.0 when both are empty (ct/spectral.py:187-193)."""
+    a = np.unique(np.asarray(a, dtype=np.int64))
+    b = np.unique(np.asarray(b, dtype=np.int64))
+    union = np.union1d(a, b).size
+    if union == 0:
+        return 1.0
+    return np.intersect1d(a, b, assume_unique=True).size / union
+
+
+def selection_stability(chunk, alphas=(0.3, 0.5, 0.7), r: float = 0.15) -> dict:
+    """Jaccard overlap of the top-r selections across cutoff ratios
+    (ct/spectral.py:196-208); every ranking runs on the device scorer."""
+    picks = {a: indices_for_ratio(rank_chunk(chunk, a), r) for a in alphas}
+    out = {}
+    for i, a in enumerate(alphas):
+        for b in alphas[i + 1:]:
+            out[(a, b)] = jaccard_overlap(picks[a], picks[b])
+    return out

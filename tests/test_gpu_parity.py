@@ -529,3 +529,89 @@ def test_c_abi_select_random_orders(ct, n):
         assert k.value == kk
         assert np.array_equal(sel.cpu().numpy(), O.indices_for_ratio(order, r))
         assert np.array_equal(keep.cpu().numpy(), O.complement_for_ratio(order, r))
+
+
+# ---------------------------------------------------------------- spectrum / rope helpers
+
+@pytest.mark.parametrize("n", [1, 2, 7, 64, 1000])
+def test_rfft_irfft_seq_reference_properties(ct, n):
+    """rfft_seq / irfft_seq (ct/spectral.py:27-34,61-66): bins vs a naive DFT
+    within 1e-9, round trip within 1e-6, Parseval (the reference's own
+    acceptance properties, tests/test_spectral.py:32-36,196-204)."""
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, 2, 4)).astype(np.float32)
+    spec = ct.rfft_seq(ct.SeqTensor(x))
+    assert spec.n_freqs == n // 2 + 1 and spec.origin_len == n
+    k = np.arange(n // 2 + 1)[:, None]
+    dft = np.exp(-2j * np.pi * k * np.arange(n)[None, :] / n) @ x.reshape(n, -1).astype(np.float64)
+    assert np.max(np.abs(spec.to_complex().reshape(n // 2 + 1, -1) - dft)) < 1e-9
+    back = ct.irfft_seq(spec, n)
+    assert np.max(np.abs(back.data - x)) < 1e-6
+    w = np.full(n // 2 + 1, 2.0)
+    w[0] = 1.0
+    if n % 2 == 0:
+        w[-1] = 1.0
+    energy = (w[:, None, None] * np.abs(spec.to_complex()) ** 2).sum() / n
+    np.testing.assert_allclose(energy, (x.astype(np.float64) ** 2).sum(), rtol=1e-10)
+    with pytest.raises(ct.ShapeError):
+        ct.irfft_seq(spec, n + 1)
+
+
+@pytest.mark.parametrize("pairing", ["adjacent", "split"])
+def test_rope_rotate_f64_matches_oracle(ct, pairing):
+    """rope_rotate (ct/rope.py:47-72) returns float64: device f64 rows vs the
+    float64 restatement, numpy and torch inputs, positions up to 70000."""
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((257, 3, 16))
+    pos = rng.integers(-5, 70000, size=257)
+    params = ct.RopeParams(head_dim=16, base=500000.0, scaling=0.5, pairing=pairing)
+    want = O.rope_rotate(x, pos, O.Rope(16, 500000.0, 0.5, pairing))
+    got = ct.rope_rotate(x, pos, params)
+    assert got.dtype == np.float64
+    # cos/sin from CUDA vs libm differ by <= 1 ulp of the table entry
+    np.testing.assert_allclose(got, want, rtol=0, atol=4e-16 * np.max(np.abs(x)) * 4)
+    gt = ct.rope_rotate(torch.as_tensor(x, device="cuda"), torch.as_tensor(pos, device="cuda"),
+                        params)
+    assert gt.is_cuda and torch.equal(gt.cpu(), torch.as_tensor(got))
+    with pytest.raises(ct.ShapeError):
+        ct.rope_rotate(x[:, :, :8], pos, params)
+
+
+def test_selection_stability_matches_oracle(ct):
+    """selection_stability (ct/spectral.py:196-208) with the device scorer vs
+    the oracle's rankings and set arithmetic."""
+    rng = np.random.default_rng(12)
+    keys = [rng.standard_normal((300, 2, 8)).astype(np.float32) for _ in range(3)]
+    vals = [rng.standard_normal((300, 2, 8)).astype(np.float32) for _ in range(3)]
+    chunk = ct.KvChunk("s", tuple(ct.SeqTensor(k) for k in keys),
+                       tuple(ct.SeqTensor(v) for v in vals))
+    got = ct.selection_stability(chunk, alphas=(0.3, 0.5, 0.7), r=0.15)
+    picks = {a: O.indices_for_ratio(O.rank_chunk(keys, vals, a)[2], 0.15) for a in (0.3, 0.5, 0.7)}
+    for (a, b), v in got.items():
+        sa, sb = set(picks[a].tolist()), set(picks[b].tolist())
+        assert v == len(sa & sb) / len(sa | sb)
+
+
+def test_toy_model_drop_in_names(ct):
+    """ct.ToyModel(ct.ToyModelConfig(...)) = the reference's seeded model in
+    HBM: weights equal the oracle's draw, and config-1 selective prefill runs
+    through it within the fp32 tolerance."""
+    cfg = ct.ToyModelConfig(seed=0, n_layers=2)
+    gm = ct.ToyModel(cfg)
+    om = O.Model(O.ModelConfig(seed=0, n_layers=2))
+    w = gm.to_numpy_weights()
+    np.testing.assert_array_equal(w["embedding"], om.embedding.astype(np.float32))
+    rng = np.random.default_rng([0, 1])
+    toks = [rng.integers(0, 256, size=96) for _ in range(2)]
+    suffix = rng.integers(0, 256, size=8)
+    ochunks, chunks = [], []
+    for j, t in enumerate(toks):
+        kr, vs = O.encode_chunk_isolated(om, t)
+        ochunks.append((kr, vs, t))
+        chunks.append(ct.KvChunk(f"t{j}", tuple(ct.SeqTensor(k) for k in kr),
+                                 tuple(ct.SeqTensor(v) for v in vs), source_tokens=t))
+    ranks = [ct.rank_chunk(c) for c in chunks]
+    res = ct.selective_prefill(gm, chunks, ranks, suffix, 0.15)
+    want = O.selective_prefill(om, ochunks, [O.rank_chunk(kr, vs)[2] for kr, vs, _ in ochunks],
+                               suffix, 0.15)
+    assert O.normwise_rel(res.logits.double().cpu().numpy(), want["logits"]) < FP32_TOL
