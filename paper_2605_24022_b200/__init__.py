@@ -33,7 +33,8 @@ _LAZY = {
     "FrequencyTokenRanker": "estimators", "RatioCalibrator": "estimators",
     # serving surface: resident pool + preallocated per-request engine
     "CachePool": "cachepool", "token_row_bytes": "cachepool", "TierConfig": "pipesim",
-    "TIER_PRESETS": "pipesim", "write_ctkv": "ctkv", "read_ctkv": "ctkv",
+    "TIER_PRESETS": "pipesim", "save_tier_config": "pipesim", "load_tier_config": "pipesim",
+    "resolve_tier": "pipesim", "write_ctkv": "ctkv", "read_ctkv": "ctkv",
     "KvPool": "pool", "SelectivePrefillEngine": "pipeline", "FullPrefillEngine": "pipeline",
     "prepare_pool": "offline", "calibrate": "scheduler", "SearchConfig": "scheduler",
     "HardwareProfile": "scheduler",

@@ -127,3 +127,29 @@ def test_transfer_cost_matches_reference_model(tmp_path):
     import pytest
     with pytest.raises(InvalidParam):
         transfer_cost_per_token(disk, 0, bpt)
+
+
+def test_tier_config_files_round_trip(tmp_path):
+    """save/load_tier_config + resolve_tier (ct/cachepool.py:100-145)."""
+    from paper_2605_24022_b200.errors import InvalidParam
+    from paper_2605_24022_b200.pipesim import (TIER_PRESETS, TierConfig, load_tier_config,
+                                               resolve_tier, save_tier_config)
+    tier = TierConfig("ssd", read_bw=535e6, write_bw=445e6, fixed_latency=2e-4,
+                      backing=str(tmp_path / "pool"))
+    path = tmp_path / "tier.cfg"
+    save_tier_config(tier, path)
+    assert path.read_text().splitlines() == [
+        "kind=ssd", "read_bw_bytes=535000000", "write_bw_bytes=445000000",
+        "fixed_latency_s=0.0002", f"backing={tmp_path / 'pool'}"]
+    assert load_tier_config(path) == tier
+    assert resolve_tier(str(path)) == tier
+    assert resolve_tier("hdd") == TIER_PRESETS["hdd"]
+    (tmp_path / "bad.cfg").write_text("# c\nkind=ssd\nread_bw_bytes 5\n")
+    import pytest
+    with pytest.raises(InvalidParam):
+        load_tier_config(tmp_path / "bad.cfg")
+    (tmp_path / "short.cfg").write_text("kind=ssd\n")
+    with pytest.raises(InvalidParam):
+        load_tier_config(tmp_path / "short.cfg")
+    with pytest.raises(InvalidParam):
+        resolve_tier("nvram")
