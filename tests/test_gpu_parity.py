@@ -615,3 +615,34 @@ def test_toy_model_drop_in_names(ct):
     want = O.selective_prefill(om, ochunks, [O.rank_chunk(kr, vs)[2] for kr, vs, _ in ochunks],
                                suffix, 0.15)
     assert O.normwise_rel(res.logits.double().cpu().numpy(), want["logits"]) < FP32_TOL
+
+
+@pytest.mark.parametrize("lengths, r", [((100, 37, 250), 0.15), ((1, 64, 3), 0.5),
+                                        ((2048, 5, 700), 0.05)])
+def test_ragged_chunks_selective_prefill_vs_oracle(ct, lengths, r):
+    """Chunks of different lengths (incl. a 1-token chunk and a non-power-of-two
+    FFT length): selections bit-exact per chunk and the fp32 mode within 1e-5
+    of the oracle (ct/toymodel.py:223-311 takes any chunk sizes)."""
+    om = O.Model(O.ModelConfig(seed=4, n_layers=2, mlp=True))
+    gm = ct.GpuModel.from_reference(om, dtype=torch.float32)
+    rng = np.random.default_rng(sum(lengths))
+    toks = [rng.integers(0, 256, size=n) for n in lengths]
+    suffix = rng.integers(0, 256, size=12)
+    ochunks, chunks = [], []
+    for j, t in enumerate(toks):
+        kr, vs = O.encode_chunk_isolated(om, t)
+        ochunks.append((kr, vs, t))
+        chunks.append(ct.KvChunk(f"g{j}", tuple(ct.SeqTensor(k) for k in kr),
+                                 tuple(ct.SeqTensor(v) for v in vs), source_tokens=t))
+    ranks = [ct.rank_chunk(c) for c in chunks]
+    aggs = [O.rank_chunk(kr, vs)[2] for kr, vs, _ in ochunks]
+    for rk, agg in zip(ranks, aggs):
+        assert np.array_equal(rk.aggregate_order, agg)
+    res = ct.selective_prefill(gm, chunks, ranks, suffix, r)
+    want = O.selective_prefill(om, ochunks, aggs, suffix, r)
+    assert np.array_equal(res.query_positions, want["query_positions"])
+    assert O.normwise_rel(res.logits.double().cpu().numpy(), want["logits"]) < FP32_TOL
+    for l in range(2):
+        K, V = res.kv[l]
+        assert O.normwise_rel(K.cpu().numpy(), want["kv"][l][0]) < FP32_TOL
+        assert O.normwise_rel(V.cpu().numpy(), want["kv"][l][1]) < FP32_TOL
