@@ -1,0 +1,79 @@
+"""Parity at BASELINE config-3 size (Mistral-7B geometry, 32 layers, 32 x 2048
+chunks + 64 suffix = 64K context, r = 0.15) through size-independent
+properties (the float64 oracle cannot run this request):
+
+* the device selection plan == the reference's integer rules on the orders;
+* pool resident in pinned host memory (the sparse H2D path config 3 is about)
+  == pool in HBM, first-token logits and every layer's blended cache bit for
+  bit;
+* r = 1 selective prefill == full-recompute prefill at 65,600 tokens, bit for
+  bit (same kernels, every token recomputed)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import cachetune_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+C, N, S, R = 32, 2048, 64, 0.15
+
+
+@pytest.fixture(scope="module")
+def big3():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2605_24022_b200 as ct
+    torch.cuda.empty_cache()
+    cfg = ct.ModelConfig.mistral_7b(n_layers=32, seed=13)
+    m = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(13)
+    toks = [rng.integers(0, cfg.vocab_size, size=N) for _ in range(C)]
+    chunks = [ct.encode_chunk_isolated(m, t, chunk_id=f"m{j}") for j, t in enumerate(toks)]
+    ranks = ct.rank_chunks(chunks)
+    suffix = torch.as_tensor(rng.integers(0, cfg.vocab_size, size=S).astype(np.int32),
+                             device="cuda")
+    yield ct, m, toks, chunks, ranks, suffix
+    del m, chunks
+    torch.cuda.empty_cache()
+
+
+def test_cfg3_pinned_pool_equals_hbm_pool_and_plan(big3):
+    ct, m, toks, chunks, ranks, suffix = big3
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    hbm = SelectivePrefillEngine(m, KvPool(chunks, ranks, "hbm"), R, S)
+    want = hbm.step(suffix).clone()
+    torch.cuda.synchronize()
+    rec = np.concatenate([O.indices_for_ratio(rk.aggregate_order, R) + j * N
+                          for j, rk in enumerate(ranks)])
+    keep = np.concatenate([O.complement_for_ratio(rk.aggregate_order, R) + j * N
+                           for j, rk in enumerate(ranks)])
+    k = O.selection_count(R, N)
+    assert np.array_equal(hbm.positions[:C * k].cpu().numpy(), rec)
+    assert np.array_equal(hbm.keep.cpu().numpy(), keep)
+    cache_hbm = hbm.cache.clone()
+    del hbm
+    torch.cuda.empty_cache()
+    pin = SelectivePrefillEngine(m, KvPool(chunks, ranks, "pinned"), R, S)
+    got = pin.step(suffix)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want)
+    assert torch.equal(pin.cache, cache_hbm)
+    del pin, cache_hbm
+    torch.cuda.empty_cache()
+
+
+def test_cfg3_r1_equals_full_prefill(big3):
+    ct, m, toks, chunks, ranks, suffix = big3
+    from paper_2605_24022_b200.pipeline import FullPrefillEngine, SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    sel = SelectivePrefillEngine(m, KvPool(chunks, ranks, "hbm"), 1.0, S)
+    got = sel.step(suffix).clone()
+    del sel
+    torch.cuda.empty_cache()
+    full = FullPrefillEngine(m, C * N + S)
+    tokens = torch.cat([torch.as_tensor(np.concatenate(toks).astype(np.int32), device="cuda"),
+                        suffix])
+    assert torch.equal(got, full.step(tokens))
