@@ -328,6 +328,42 @@ __device__ __forceinline__ void dft16(cpx<T>* v) {
   }
 }
 
+// Forward radix-8 DFT -> low band of the default alpha = 0.5 at N = 2048
+// (cutoff N/4: of the bins k = j + 256 r only r = 0, 1, 6, 7 survive, r = 6
+// not at j = 0) -> inverse radix-8 DFT, without computing the masked outputs
+// or multiplying by the zeroed inputs.  Same DFT definitions as dft_small<8>.
+template <typename T>
+__device__ __forceinline__ void lowband8_fwd_inv(cpx<T>* w, bool zero6) {
+  const T h = (T)0.70710678118654752440;
+  // forward, decimation in frequency: even outputs from a, odd from b
+  const cpx<T> a0 = cadd(w[0], w[4]), a1 = cadd(w[1], w[5]);
+  const cpx<T> a2 = cadd(w[2], w[6]), a3 = cadd(w[3], w[7]);
+  const cpx<T> b0 = csub(w[0], w[4]);
+  const cpx<T> b1 = cmul(csub(w[1], w[5]), cpx<T>{h, -h});
+  const cpx<T> b2 = mul_mi<false>(csub(w[2], w[6]));
+  const cpx<T> b3 = cmul(csub(w[3], w[7]), cpx<T>{-h, -h});
+  const cpx<T> y0 = cadd(cadd(a0, a2), cadd(a1, a3));
+  cpx<T> y6 = cadd(csub(a0, a2), mul_mi<true>(csub(a1, a3)));   // + i (a1 - a3)
+  const cpx<T> y1 = cadd(cadd(b0, b2), cadd(b1, b3));
+  const cpx<T> y7 = cadd(csub(b0, b2), mul_mi<true>(csub(b1, b3)));
+  if (zero6) y6 = cpx<T>{(T)0, (T)0};
+  // inverse from bins 0, 1, 6, 7: E_p = y0 + (-i)^p y6, O_p = y1 + (-i)^p y7
+  const cpx<T> e0 = cadd(y0, y6), e2 = csub(y0, y6);
+  const cpx<T> e1 = cadd(y0, mul_mi<false>(y6)), e3 = cadd(y0, mul_mi<true>(y6));
+  const cpx<T> o0 = cadd(y1, y7), o2 = csub(y1, y7);
+  const cpx<T> o1 = cmul(cadd(y1, mul_mi<false>(y7)), cpx<T>{h, h});
+  const cpx<T> o3 = cmul(cadd(y1, mul_mi<true>(y7)), cpx<T>{-h, h});
+  const cpx<T> o2i = mul_mi<true>(o2);
+  w[0] = cadd(e0, o0);
+  w[4] = csub(e0, o0);
+  w[1] = cadd(e1, o1);
+  w[5] = csub(e1, o1);
+  w[2] = cadd(e2, o2i);
+  w[6] = csub(e2, o2i);
+  w[3] = cadd(e3, o3);
+  w[7] = csub(e3, o3);
+}
+
 template <int R, bool INV, typename T>
 __device__ __forceinline__ void dft_r(cpx<T>* v) {
   if constexpr (R == 16) dft16<INV>(v);
@@ -443,7 +479,9 @@ __device__ __forceinline__ void load_tile(IN* tile, const IN* base, int64_t ld_t
   cp_async_commit();
 }
 
-template <typename T, typename IN, int R3, int SPT>
+// LB: the default band (alpha = 0.5 at N = 2048, cutoff N/4) with the pruned
+// radix-8 middle passes (lowband8_fwd_inv).
+template <typename T, typename IN, int R3, int SPT, bool LB = false>
 __global__ void __launch_bounds__(FFT2_THREADS / SPT, 1)
 fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int L, int lanes,
                    int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff,
@@ -568,14 +606,18 @@ fft2_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, i
         } else {
           twiddle<R3, false, N>(w, tw, j);
         }
-        dft_r<R3, false>(w);
+        if constexpr (LB && R3 == 8) {
+          lowband8_fwd_inv(w, j == 0);
+        } else {
+          dft_r<R3, false>(w);
 #pragma unroll
-        for (int r = 0; r < R3; ++r) {
-          const int k = j + NR3 * r;
-          const int kk = k < N - k ? k : N - k;
-          if (cutoff >= 0 ? kk >= cutoff : kk < -cutoff - 1) w[r] = {(T)0, (T)0};
+          for (int r = 0; r < R3; ++r) {
+            const int k = j + NR3 * r;
+            const int kk = k < N - k ? k : N - k;
+            if (cutoff >= 0 ? kk >= cutoff : kk < -cutoff - 1) w[r] = {(T)0, (T)0};
+          }
+          dft_r<R3, true>(w);
         }
-        dft_r<R3, true>(w);
       }
     }
     group_sync<GT>(g);
@@ -1098,13 +1140,15 @@ static int launch_fft_t(const void* k, const void* v, int L, int C, int lanes, i
 // N = 2048: two signals per thread (8 warps, 254 registers) measured 4 % (f64) /
 // 7 % (f32) faster than one signal per thread (16 warps, 128 registers)
 static int g_fft2_spt = getenv("CT_SCORER_SPT") ? atoi(getenv("CT_SCORER_SPT")) : 2;
+// CT_SCORER_NO_LB=1: generic masked middle passes even for the default band
+static bool g_fft2_no_lb = getenv("CT_SCORER_NO_LB") != nullptr;
 
-template <typename T, typename IN, int R3, int SPT>
+template <typename T, typename IN, int R3, int SPT, bool LB = false>
 static int launch_fft2_spt(const void* k, const void* v, int L, int C, int lanes, int64_t ldt,
                            int64_t ldl, int64_t ldc, int cutoff, const void* tw, double* partial,
                            cudaStream_t st) {
   using Cfg = Fft2Cfg<T, IN, R3, SPT>;
-  auto kern = fft2_energy_kernel<T, IN, R3, SPT>;
+  auto kern = fft2_energy_kernel<T, IN, R3, SPT, LB>;
   CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
   const int nlb = (lanes + LANE_BLOCK - 1) / LANE_BLOCK;
   dim3 grid(nlb, 2, C * L);
@@ -1117,8 +1161,12 @@ template <typename T, typename IN, int R3>
 static int launch_fft2_t(const void* k, const void* v, int L, int C, int lanes, int64_t ldt,
                          int64_t ldl, int64_t ldc, int cutoff, const void* tw, double* partial,
                          cudaStream_t st) {
-  if (R3 == 8 && g_fft2_spt == 2)
+  if (R3 == 8 && g_fft2_spt == 2) {
+    if (cutoff == 256 * R3 / 4 && !g_fft2_no_lb)
+      return launch_fft2_spt<T, IN, R3, 2, true>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw,
+                                                 partial, st);
     return launch_fft2_spt<T, IN, R3, 2>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
+  }
   return launch_fft2_spt<T, IN, R3, 1>(k, v, L, C, lanes, ldt, ldl, ldc, cutoff, tw, partial, st);
 }
 
