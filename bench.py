@@ -555,20 +555,34 @@ def run_batch(args, rank, world, local_rank):
         docs = [int(x) for x in rng.choice(c["corpus"], size=c["chunks"], replace=False)]
         suf = rng.integers(0, cfg.vocab_size, size=c["suffix"]).astype(np.int32)
         reqs[i] = (docs, torch.as_tensor(suf, device=dev), torch.as_tensor(suf).pin_memory())
-    eng = SelectivePrefillEngine(model, pool, c["r"], c["suffix"], n_chunks=c["chunks"])
+    # CT_CFG5_STREAMS=k: k engines on k streams, requests dealt round-robin, so
+    # one request's HBM-bound kernels can overlap another's tensor-core work
+    n_streams = max(1, int(os.environ.get("CT_CFG5_STREAMS", "1")))
+    engines = [SelectivePrefillEngine(model, pool, c["r"], c["suffix"], n_chunks=c["chunks"])
+               for _ in range(n_streams)]
+    eng = engines[0]
+    streams = [torch.cuda.current_stream(dev)] if n_streams == 1 else \
+        [torch.cuda.Stream(device=dev) for _ in range(n_streams)]
     logits_host = {i: torch.empty((1, cfg.vocab_size), dtype=torch.float32).pin_memory()
                    for i in mine}
 
     def batch(e2e=False, out=None):
-        for i in mine:
+        main = torch.cuda.current_stream(dev)
+        for st in streams:
+            st.wait_stream(main)
+        for idx, i in enumerate(mine):
             docs, sd, sh = reqs[i]
-            eng.bind(docs)
-            if e2e:
-                eng.step(sh, logits_host[i])
-            else:
-                lg = eng.step(sd)
-                if out is not None:
-                    out[i] = lg
+            e = engines[idx % n_streams]
+            with torch.cuda.stream(streams[idx % n_streams]):
+                e.bind(docs)
+                if e2e:
+                    e.step(sh, logits_host[i])
+                else:
+                    lg = e.step(sd)
+                    if out is not None:
+                        out[i] = lg
+        for st in streams:
+            main.wait_stream(st)
     for _ in range(args.warmup):
         batch()
     torch.cuda.synchronize()
@@ -637,7 +651,7 @@ def run_batch(args, rank, world, local_rank):
                 "encoded on the GPU by the same model)",
         "config": {"workload": c["desc"], "parallelism": f"replicas x{world} (request-level)",
                    "numa_bind": (f"{len(numa_cpus)} GPU-local cpus" if numa_cpus else None),
-                   "requests_per_step": n_req, "requests_on_rank0": len(mine),
+                   "requests_per_step": n_req, "requests_on_rank0": len(mine), "streams": n_streams,
                    "l2": "inputs larger than L2 (17 GB corpus + 16 GB weights); no flush"},
         "e2e": {"value": n_req * args.steps / (e2e_total * 1e-3), "unit": "requests/s",
                 "h2d_bytes_per_step": n_req * 4 * (c["suffix"] + c["chunks"]),
