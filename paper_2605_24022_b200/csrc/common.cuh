@@ -57,6 +57,14 @@ __device__ __forceinline__ uint4 ldg_stream(const uint4* p) {
   return r;
 }
 
+__device__ __forceinline__ float4 ldg_stream_f4(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
 inline bool valid_dtype(int d) { return d == CT_F32 || d == CT_BF16; }
 inline size_t dtype_size(int d) { return d == CT_BF16 ? 2 : (d == CT_F64 ? 8 : 4); }
 

@@ -2,6 +2,8 @@
 // (ct/toymodel.py:149), fused residual add + RMSNorm (ct/toymodel.py:88-89,
 // :156, :184) and the MLP activation (ct/toymodel.py:186 ReLU; SwiGLU for the
 // Llama geometry).  Plus the library's version / error / transfer helpers.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace ct {
@@ -52,8 +54,8 @@ residual_rmsnorm_kernel(float* __restrict__ h, const TD* __restrict__ delta, int
 
 // Vectorised residual + RMSNorm: one CTA per row, the row held in registers
 // (float4 per thread-slot), so h and delta are read once and h, x written once.
-template <int VPT, typename TX>
-__global__ void __launch_bounds__(256)
+template <int VPT, typename TX, int NT = 256>
+__global__ void __launch_bounds__(NT)
 residual_rmsnorm_vec_kernel(float* __restrict__ h, const float* __restrict__ delta, int64_t cols,
                             double eps, TX* __restrict__ x) {
   const int64_t row = blockIdx.x;
@@ -64,7 +66,7 @@ residual_rmsnorm_vec_kernel(float* __restrict__ h, const float* __restrict__ del
   float ss = 0.f;
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * 256;
+    const int c = threadIdx.x + i * NT;
     if (c < nv) {
       float4 a = hr[c];
       if (dr) {
@@ -76,17 +78,17 @@ residual_rmsnorm_vec_kernel(float* __restrict__ h, const float* __restrict__ del
       ss += a.x * a.x + a.y * a.y + a.z * a.z + a.w * a.w;
     }
   }
-  __shared__ float red[8];
+  __shared__ float red[NT / 32];
   for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   float tot = 0.f;
 #pragma unroll
-  for (int w = 0; w < 8; ++w) tot += red[w];
+  for (int w = 0; w < NT / 32; ++w) tot += red[w];
   const float inv = (float)(1.0 / sqrt((double)tot / (double)cols + eps));
 #pragma unroll
   for (int i = 0; i < VPT; ++i) {
-    const int c = threadIdx.x + i * 256;
+    const int c = threadIdx.x + i * NT;
     if (c < nv) {
       TX* xo = x + row * cols + 4 * (int64_t)c;
       if constexpr (sizeof(TX) == 2) {
@@ -101,6 +103,59 @@ residual_rmsnorm_vec_kernel(float* __restrict__ h, const float* __restrict__ del
                                                      v[i].w * inv);
       }
     }
+  }
+}
+
+// RMSNorm without a residual (the residual add lives in the GEMM epilogues):
+// a CTA walks rows r, r + gridDim, ... keeping the next row's h in registers
+// while it reduces and stores the current one.
+template <int VPT, typename TX>
+__global__ void __launch_bounds__(256)
+rmsnorm_rows_kernel(const float* __restrict__ h, int64_t A, double eps, TX* __restrict__ x) {
+  constexpr int COLS = 4 * 256 * VPT;
+  __shared__ float red[2][8];
+  float4 cur[VPT], nxt[VPT];
+  int64_t row = blockIdx.x;
+  if (row >= A) return;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i)
+    cur[i] = ldg_stream_f4(reinterpret_cast<const float4*>(h + row * COLS) + threadIdx.x + i * 256);
+  for (int par = 0; row < A; row += gridDim.x, par ^= 1) {
+    const int64_t nrow = row + gridDim.x;
+    if (nrow < A) {
+#pragma unroll
+      for (int i = 0; i < VPT; ++i)
+        nxt[i] = ldg_stream_f4(reinterpret_cast<const float4*>(h + nrow * COLS) + threadIdx.x +
+                               i * 256);
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < VPT; ++i)
+      ss += cur[i].x * cur[i].x + cur[i].y * cur[i].y + cur[i].z * cur[i].z + cur[i].w * cur[i].w;
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[par][threadIdx.x >> 5] = ss;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[par][w];
+    const float inv = (float)(1.0 / sqrt((double)tot / (double)COLS + eps));
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      TX* xo = x + row * COLS + 4 * (int64_t)(threadIdx.x + i * 256);
+      if constexpr (sizeof(TX) == 2) {
+        __nv_bfloat162 lo = __floats2bfloat162_rn(cur[i].x * inv, cur[i].y * inv);
+        __nv_bfloat162 hi = __floats2bfloat162_rn(cur[i].z * inv, cur[i].w * inv);
+        uint2 u;
+        u.x = *reinterpret_cast<uint32_t*>(&lo);
+        u.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(xo) = u;
+      } else {
+        *reinterpret_cast<float4*>(xo) = make_float4(cur[i].x * inv, cur[i].y * inv,
+                                                     cur[i].z * inv, cur[i].w * inv);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) cur[i] = nxt[i];
   }
 }
 
@@ -127,6 +182,32 @@ __global__ void swiglu_vec_kernel(const uint4* __restrict__ gu, int64_t A, int64
     act[t] = o;
   }
 }
+
+// One 16-byte group of 8 outputs per thread, rows on blockIdx.y: no 64-bit
+// division per element, and enough CTAs resident that every SM keeps ~64 KB
+// of gate/up loads in flight.
+__global__ void __launch_bounds__(256)
+swiglu_row_kernel(const uint4* __restrict__ gu, int64_t inter8, uint4* __restrict__ act) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= inter8) return;
+  const int64_t a = blockIdx.y;
+  const uint4 g = ldg_stream(gu + a * 2 * inter8 + i);
+  const uint4 u = ldg_stream(gu + a * 2 * inter8 + inter8 + i);
+  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+  const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+  uint4 o;
+  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float2 gf = __bfloat1622float2(g2[k]);
+    const float2 uf = __bfloat1622float2(u2[k]);
+    o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
+                                  gf.y / (1.f + __expf(-gf.y)) * uf.y);
+  }
+  act[a * inter8 + i] = o;
+}
+
+static const bool g_swiglu_v1 = getenv("CT_SWIGLU_V1") != nullptr;
 
 template <typename TI, typename TO>
 __global__ void mlp_act_kernel(const TI* __restrict__ gu, int64_t A, int64_t inter, int kind,
@@ -184,6 +265,8 @@ extern "C" int ct_embedding_gather(const float* table, const int32_t* tokens, in
   return check_launch("embedding_kernel");
 }
 
+static const bool g_rms_v1 = getenv("CT_RMS_V1") != nullptr;
+
 extern "C" int ct_residual_rmsnorm(float* h, const void* delta, int delta_dtype, int64_t A,
                                    int64_t cols, double eps, void* x_out, int x_dtype,
                                    void* stream) {
@@ -193,6 +276,17 @@ extern "C" int ct_residual_rmsnorm(float* h, const void* delta, int delta_dtype,
   const unsigned g = (unsigned)A;
   const bool aligned = ((uintptr_t)h % 16 == 0) && ((uintptr_t)delta % 16 == 0) &&
                        ((uintptr_t)x_out % 16 == 0) && x_out != nullptr;
+  // no residual, rows of 4 * 256 * VPT f32 -> x: persistent row loop with the
+  // next row's loads issued before this row's reduction and stores
+  if (delta == nullptr && cols == 4 * 256 * 4 && aligned && !g_rms_v1) {
+    // 3..16 CTAs per SM measured flat (22.6 us for 4992 x 4096)
+    const unsigned grid = (unsigned)std::min<int64_t>(A, 148 * 6);
+    if (x_dtype == CT_BF16)
+      rmsnorm_rows_kernel<4, __nv_bfloat16><<<grid, 256, 0, st>>>(h, A, eps, (__nv_bfloat16*)x_out);
+    else
+      rmsnorm_rows_kernel<4, float><<<grid, 256, 0, st>>>(h, A, eps, (float*)x_out);
+    return check_launch("rmsnorm_rows_kernel");
+  }
   if (delta_dtype == CT_F32 && cols % 4 == 0 && cols <= 4 * 256 * 8 && aligned) {
     const int vpt = (int)((cols / 4 + 255) / 256);
 #define CT_RMS(V)                                                                                  \
@@ -228,6 +322,12 @@ extern "C" int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype
   const unsigned g = grid_cap(A * inter);
   if (kind == 0 && in_dtype == CT_BF16 && act_dtype == CT_BF16 && inter % 8 == 0 &&
       ((uintptr_t)gu % 16 == 0) && ((uintptr_t)act % 16 == 0)) {
+    if (!g_swiglu_v1 && A <= 65535) {
+      const int64_t inter8 = inter / 8;
+      swiglu_row_kernel<<<dim3((unsigned)((inter8 + 255) / 256), (unsigned)A), 256, 0, st>>>(
+          (const uint4*)gu, inter8, (uint4*)act);
+      return check_launch("swiglu_row_kernel");
+    }
     swiglu_vec_kernel<<<grid_cap(A * inter / 8), 256, 0, st>>>((const uint4*)gu, A, inter / 8,
                                                                 (uint4*)act);
     return check_launch("swiglu_vec_kernel");

@@ -86,6 +86,37 @@ def main():
     ms = ev_time(qkv, 50)
     nbytes = A * hpr * D * 2 * 2 + A * H * D * 2
     print(f"qkv:   {ms * 1e3:.1f} us  {nbytes / ms / 1e6:.0f} GB/s  ({nbytes / 1e6:.1f} MB)")
+    del qkvs, qouts, kraws, pools, caches
+    torch.cuda.empty_cache()
+
+    # SwiGLU: gate|up [A, 2*inter] bf16 -> act [A, inter] bf16
+    inter, hid = 14336, 4096
+    gus = [torch.randn((A, 2 * inter), device=dev).to(torch.bfloat16) for _ in range(COPIES)]
+    acts = [torch.empty((A, inter), dtype=torch.bfloat16, device=dev) for _ in range(COPIES)]
+
+    def swiglu(i):
+        j = i % COPIES
+        _lib.call("ct_mlp_act", _dev.ptr(gus[j]), A, inter, _dev.ct_dtype(torch.bfloat16), 0,
+                  _dev.ptr(acts[j]), _dev.ct_dtype(torch.bfloat16), st)
+
+    ms = ev_time(swiglu, 50)
+    nbytes = A * inter * 2 * 3
+    print(f"swiglu: {ms * 1e3:.1f} us  {nbytes / ms / 1e6:.0f} GB/s  ({nbytes / 1e6:.1f} MB)")
+    del gus, acts
+    torch.cuda.empty_cache()
+
+    # rmsnorm: h [A, hid] f32 -> x [A, hid] bf16
+    hs = [torch.randn((A, hid), device=dev) for _ in range(COPIES * 4)]
+    xs = [torch.empty((A, hid), dtype=torch.bfloat16, device=dev) for _ in range(COPIES * 4)]
+
+    def rms(i):
+        j = i % (COPIES * 4)
+        _lib.call("ct_residual_rmsnorm", _dev.ptr(hs[j]), None, _lib.CT_F32, A, hid, 1e-6,
+                  _dev.ptr(xs[j]), _dev.ct_dtype(torch.bfloat16), st)
+
+    ms = ev_time(rms, 100)
+    nbytes = A * hid * (4 + 2)
+    print(f"rmsnorm: {ms * 1e3:.1f} us  {nbytes / ms / 1e6:.0f} GB/s  ({nbytes / 1e6:.1f} MB)")
 
 
 if __name__ == "__main__":
