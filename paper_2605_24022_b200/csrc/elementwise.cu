@@ -186,25 +186,29 @@ __global__ void swiglu_vec_kernel(const uint4* __restrict__ gu, int64_t A, int64
 // One 16-byte group of 8 outputs per thread, rows on blockIdx.y: no 64-bit
 // division per element, and enough CTAs resident that every SM keeps ~64 KB
 // of gate/up loads in flight.
+template <bool LOOP>
 __global__ void __launch_bounds__(256)
-swiglu_row_kernel(const uint4* __restrict__ gu, int64_t inter8, uint4* __restrict__ act) {
+swiglu_row_kernel(const uint4* __restrict__ gu, int64_t A, int64_t inter8,
+                  uint4* __restrict__ act) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= inter8) return;
-  const int64_t a = blockIdx.y;
-  const uint4 g = ldg_stream(gu + a * 2 * inter8 + i);
-  const uint4 u = ldg_stream(gu + a * 2 * inter8 + inter8 + i);
-  const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
-  const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
-  uint4 o;
-  __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float2 gf = __bfloat1622float2(g2[k]);
-    const float2 uf = __bfloat1622float2(u2[k]);
-    o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
-                                  gf.y / (1.f + __expf(-gf.y)) * uf.y);
+  // LOOP only when A exceeds one grid dimension (65535 rows)
+  for (int64_t a = blockIdx.y; LOOP ? a < A : a == blockIdx.y; a += gridDim.y) {
+    const uint4 g = ldg_stream(gu + a * 2 * inter8 + i);
+    const uint4 u = ldg_stream(gu + a * 2 * inter8 + inter8 + i);
+    const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&g);
+    const __nv_bfloat162* u2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint4 o;
+    __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&o);
+  #pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const float2 gf = __bfloat1622float2(g2[k]);
+      const float2 uf = __bfloat1622float2(u2[k]);
+      o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
+                                    gf.y / (1.f + __expf(-gf.y)) * uf.y);
+    }
+    act[a * inter8 + i] = o;
   }
-  act[a * inter8 + i] = o;
 }
 
 static const bool g_swiglu_v1 = getenv("CT_SWIGLU_V1") != nullptr;
@@ -322,10 +326,14 @@ extern "C" int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype
   const unsigned g = grid_cap(A * inter);
   if (kind == 0 && in_dtype == CT_BF16 && act_dtype == CT_BF16 && inter % 8 == 0 &&
       ((uintptr_t)gu % 16 == 0) && ((uintptr_t)act % 16 == 0)) {
-    if (!g_swiglu_v1 && A <= 65535) {
+    if (!g_swiglu_v1) {
       const int64_t inter8 = inter / 8;
-      swiglu_row_kernel<<<dim3((unsigned)((inter8 + 255) / 256), (unsigned)A), 256, 0, st>>>(
-          (const uint4*)gu, inter8, (uint4*)act);
+      const unsigned gy = (unsigned)std::min<int64_t>(A, 65535);
+      const dim3 grid((unsigned)((inter8 + 255) / 256), gy);
+      if (A <= 65535)
+        swiglu_row_kernel<false><<<grid, 256, 0, st>>>((const uint4*)gu, A, inter8, (uint4*)act);
+      else
+        swiglu_row_kernel<true><<<grid, 256, 0, st>>>((const uint4*)gu, A, inter8, (uint4*)act);
       return check_launch("swiglu_row_kernel");
     }
     swiglu_vec_kernel<<<grid_cap(A * inter / 8), 256, 0, st>>>((const uint4*)gu, A, inter / 8,

@@ -105,3 +105,29 @@ def test_qkv_bf16_fast_path(ct, Hq, Hkv, D):
     assert torch.equal(kraw, x[:, Hq:Hq + Hkv])
     _close_bf16(cache[0, pos.long()], _rotate_ref(x[:, Hq:Hq + Hkv], pos, table))
     assert torch.equal(cache[1, pos.long()], x[:, Hq + Hkv:])
+
+
+@pytest.mark.parametrize("A, inter", [(1, 64), (3, 14336), (70000, 64)])
+def test_swiglu_and_rmsnorm_kernels_vs_torch(A, inter):
+    """ct_mlp_act (SwiGLU, rows on blockIdx.y incl. more rows than one grid
+    dimension holds) and ct_residual_rmsnorm (persistent row loop at hid 4096)
+    vs PyTorch fp32 of the same op, one bf16 rounding apart."""
+    from paper_2605_24022_b200 import _dev, _lib
+    torch.manual_seed(A)
+    gu = torch.randn((A, 2 * inter), device="cuda").to(torch.bfloat16)
+    act = torch.empty((A, inter), dtype=torch.bfloat16, device="cuda")
+    _lib.call("ct_mlp_act", gu.data_ptr(), A, inter, _lib.CT_BF16, 0, act.data_ptr(),
+              _lib.CT_BF16, _dev.stream_handle())
+    g, u = gu[:, :inter].float(), gu[:, inter:].float()
+    want = (g * torch.sigmoid(g) * u)
+    err = (act.float() - want).abs()
+    assert bool((err <= want.abs() * 2.0 ** -7 + 1e-6).all())
+    if A <= 3:
+        return
+    hid = 4096
+    h = torch.randn((A // 10, hid), device="cuda")
+    x = torch.empty((A // 10, hid), dtype=torch.bfloat16, device="cuda")
+    _lib.call("ct_residual_rmsnorm", h.data_ptr(), None, _lib.CT_F32, A // 10, hid, 1e-6,
+              x.data_ptr(), _lib.CT_BF16, _dev.stream_handle())
+    ref = h.double() / torch.sqrt((h.double() ** 2).mean(dim=1, keepdim=True) + 1e-6)
+    assert bool(((x.double() - ref).abs() <= ref.abs() * 2.0 ** -8 + 1e-6).all())
