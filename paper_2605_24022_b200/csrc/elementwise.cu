@@ -186,7 +186,14 @@ __global__ void swiglu_vec_kernel(const uint4* __restrict__ gu, int64_t A, int64
 // One 16-byte group of 8 outputs per thread, rows on blockIdx.y: no 64-bit
 // division per element, and enough CTAs resident that every SM keeps ~64 KB
 // of gate/up loads in flight.
-template <bool LOOP>
+__device__ __forceinline__ float silu_tanh(float g) {
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * g));
+  const float hg = 0.5f * g;
+  return fmaf(hg, t, hg);
+}
+
+template <bool LOOP, bool TANH = true>
 __global__ void __launch_bounds__(256)
 swiglu_row_kernel(const uint4* __restrict__ gu, int64_t A, int64_t inter8,
                   uint4* __restrict__ act) {
@@ -204,14 +211,21 @@ swiglu_row_kernel(const uint4* __restrict__ gu, int64_t A, int64_t inter8,
     for (int k = 0; k < 4; ++k) {
       const float2 gf = __bfloat1622float2(g2[k]);
       const float2 uf = __bfloat1622float2(u2[k]);
-      o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
-                                    gf.y / (1.f + __expf(-gf.y)) * uf.y);
+      // silu(g) = g sigmoid(g) = 0.5 g (1 + tanh(g / 2)): one MUFU op per
+      // element instead of ex2 + rcp (the kernel is MUFU-co-bound at the
+      // power-capped step clock); tanh.approx error ~2^-11, output is bf16
+      if constexpr (TANH)
+        o2[k] = __floats2bfloat162_rn(silu_tanh(gf.x) * uf.x, silu_tanh(gf.y) * uf.y);
+      else
+        o2[k] = __floats2bfloat162_rn(gf.x / (1.f + __expf(-gf.x)) * uf.x,
+                                      gf.y / (1.f + __expf(-gf.y)) * uf.y);
     }
     act[a * inter8 + i] = o;
   }
 }
 
 static const bool g_swiglu_v1 = getenv("CT_SWIGLU_V1") != nullptr;
+static const bool g_swiglu_exp = getenv("CT_SWIGLU_EXP") != nullptr;  // ex2 + rcp form
 
 template <typename TI, typename TO>
 __global__ void mlp_act_kernel(const TI* __restrict__ gu, int64_t A, int64_t inter, int kind,
@@ -330,7 +344,10 @@ extern "C" int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype
       const int64_t inter8 = inter / 8;
       const unsigned gy = (unsigned)std::min<int64_t>(A, 65535);
       const dim3 grid((unsigned)((inter8 + 255) / 256), gy);
-      if (A <= 65535)
+      if (A <= 65535 && g_swiglu_exp)
+        swiglu_row_kernel<false, false><<<grid, 256, 0, st>>>((const uint4*)gu, A, inter8,
+                                                              (uint4*)act);
+      else if (A <= 65535)
         swiglu_row_kernel<false><<<grid, 256, 0, st>>>((const uint4*)gu, A, inter8, (uint4*)act);
       else
         swiglu_row_kernel<true><<<grid, 256, 0, st>>>((const uint4*)gu, A, inter8, (uint4*)act);
