@@ -19,7 +19,8 @@
  *     matching *_workspace_bytes() query.
  *   - every call takes a cudaStream_t (passed as void*), is asynchronous and
  *     never synchronises the device.
- *   - reentrant: no mutable globals except the per-thread error string.
+ *   - reentrant: no mutable globals except the per-thread error string and
+ *     the atomic launch counters (ct_launch_stats).
  *   - token-major KV layout [token][head][dim] (ct/kvcore.py:31-66).
  */
 #ifndef CACHETUNE_B200_H
@@ -51,6 +52,13 @@ int ct_version(void);
 int ct_last_error(char* buf, size_t len);
 /* number of SMs of the current device (0 without a device) */
 int ct_device_sm_count(void);
+
+/* Launch evidence: "kernel=count;kernel=count;..." for every kernel this
+ * library launched successfully since load (or the last reset), e.g.
+ * "attention_pp_kernel=31" proves the tcgen05 attention ran.  Host-side
+ * counters only (no device sync). */
+int ct_launch_stats(char* buf, size_t len);
+void ct_launch_stats_reset(void);
 
 /* ------------------------------------------------------------------ */
 /* (1) frequency-domain scorer -- replaces ct/spectral.py:69-90

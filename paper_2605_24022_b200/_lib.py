@@ -53,6 +53,8 @@ _SIGS = {
     "ct_version": (c_int, []),
     "ct_last_error": (c_int, [ctypes.c_char_p, c_size_t]),
     "ct_device_sm_count": (c_int, []),
+    "ct_launch_stats": (c_int, [ctypes.c_char_p, c_size_t]),
+    "ct_launch_stats_reset": (None, []),
     "ct_score_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int]),
     "ct_score_chunks": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
                                 c_int64, c_int64, c_int64, c_int64, c_int, c_void_p, c_void_p,
@@ -135,9 +137,26 @@ def last_error() -> str:
     return buf.value.decode(errors="replace")
 
 
+def launch_stats() -> dict:
+    """Kernel name -> successful launches since load / the last reset, as
+    counted inside the .so (ct_launch_stats)."""
+    buf = ctypes.create_string_buffer(8192)
+    check(load().ct_launch_stats(buf, 8192), "ct_launch_stats")
+    out = {}
+    for item in buf.value.decode().split(";"):
+        if item:
+            name, _, n = item.rpartition("=")
+            out[name] = int(n)
+    return out
+
+
+def launch_stats_reset() -> None:
+    load().ct_launch_stats_reset()
+
+
 # kernel-launching entry points seen through check()/call() (bench evidence)
 LAUNCH_COUNT = {"n": 0}
-_NOT_KERNELS = {"ct_copy_ranges_h2d", "ct_host_alloc", "ct_host_free"}
+_NOT_KERNELS = {"ct_copy_ranges_h2d", "ct_host_alloc", "ct_host_free", "ct_launch_stats"}
 
 
 _DEBUG_SYNC = bool(int(__import__("os").environ.get("CT_DEBUG_SYNC", "0")))

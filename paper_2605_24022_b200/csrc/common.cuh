@@ -23,10 +23,15 @@ inline int fail(int status, const char* fmt, ...) {
   return status;
 }
 
+// Per-kernel launch counter (ct_launch_stats): `what` is the kernel name, a
+// string literal, so the table keys on its address.
+void note_launch(const char* what);
+
 inline int check_launch(const char* what) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess)
     return fail(CT_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  note_launch(what);
   return CT_OK;
 }
 

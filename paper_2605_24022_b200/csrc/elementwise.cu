@@ -3,12 +3,45 @@
 // :156, :184) and the MLP activation (ct/toymodel.py:186 ReLU; SwiGLU for the
 // Llama geometry).  Plus the library's version / error / transfer helpers.
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 
 #include "common.cuh"
 
 namespace ct {
 
 thread_local char g_last_error[512] = "";
+
+// Launch evidence: kernel name -> number of successful launches since load or
+// the last ct_launch_stats_reset.  Names are string literals (stable
+// addresses); a new name takes the table mutex once, counting is lock-free.
+namespace {
+constexpr int kMaxKernels = 96;
+std::atomic<const char*> g_kname[kMaxKernels];
+std::atomic<long long> g_kcount[kMaxKernels];
+std::atomic<int> g_knum{0};
+std::mutex g_kmutex;
+}  // namespace
+
+void note_launch(const char* what) {
+  const int n = g_knum.load(std::memory_order_acquire);
+  for (int i = 0; i < n; ++i)
+    if (g_kname[i].load(std::memory_order_relaxed) == what) {
+      g_kcount[i].fetch_add(1, std::memory_order_relaxed);
+      return;
+    }
+  std::lock_guard<std::mutex> lk(g_kmutex);
+  const int m = g_knum.load(std::memory_order_relaxed);
+  for (int i = 0; i < m; ++i)
+    if (g_kname[i].load(std::memory_order_relaxed) == what) {
+      g_kcount[i].fetch_add(1, std::memory_order_relaxed);
+      return;
+    }
+  if (m == kMaxKernels) return;
+  g_kname[m].store(what, std::memory_order_relaxed);
+  g_kcount[m].store(1, std::memory_order_relaxed);
+  g_knum.store(m + 1, std::memory_order_release);
+}
 
 __global__ void embedding_kernel(const float* __restrict__ table, const int32_t* __restrict__ tok,
                                  int64_t A, int64_t cols, float* __restrict__ out) {
@@ -264,6 +297,26 @@ extern "C" int ct_last_error(char* buf, size_t len) {
   strncpy(buf, g_last_error, len - 1);
   buf[len - 1] = 0;
   return CT_OK;
+}
+
+extern "C" int ct_launch_stats(char* buf, size_t len) {
+  if (!buf || !len) return fail(CT_ERR_PARAM, "ct_launch_stats: empty buffer");
+  size_t used = 0;
+  buf[0] = 0;
+  const int n = g_knum.load(std::memory_order_acquire);
+  for (int i = 0; i < n; ++i) {
+    const int w = snprintf(buf + used, len - used, "%s%s=%lld", i ? ";" : "",
+                           g_kname[i].load(std::memory_order_relaxed),
+                           (long long)g_kcount[i].load(std::memory_order_relaxed));
+    if (w < 0 || (size_t)w >= len - used) return fail(CT_ERR_PARAM, "ct_launch_stats: buffer too small");
+    used += (size_t)w;
+  }
+  return CT_OK;
+}
+
+extern "C" void ct_launch_stats_reset(void) {
+  const int n = g_knum.load(std::memory_order_acquire);
+  for (int i = 0; i < n; ++i) g_kcount[i].store(0, std::memory_order_relaxed);
 }
 
 extern "C" int ct_device_sm_count(void) {

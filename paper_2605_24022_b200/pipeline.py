@@ -188,6 +188,17 @@ class SelectivePrefillEngine:
         else:
             self._ev("forward", l, 1).record()
 
+    def _step_hook(self, user):
+        if not self.record_timeline:
+            return user
+        if user is None:
+            return self._hook
+
+        def both(l, phase):
+            self._hook(l, phase)
+            user(l, phase)
+        return both
+
     def timeline(self):
         """Timeline of the last step recorded with record_timeline=True, in
         seconds from the step start (ct/pipesim.py:93-105 schema); audit it
@@ -232,8 +243,11 @@ class SelectivePrefillEngine:
                   _dev.ptr(self.cache[l, 0]), _dev.ptr(self.cache[l, 1]), self.row_elems, st)
         self.timer.stop("blend", t)
 
-    def step(self, suffix=None, logits_out: torch.Tensor | None = None) -> torch.Tensor:
-        """One request: suffix (host pinned or device int32 [S]) -> last-row logits."""
+    def step(self, suffix=None, logits_out: torch.Tensor | None = None,
+             hook=None) -> torch.Tensor:
+        """One request: suffix (host pinned or device int32 [S]) -> last-row logits.
+        hook(layer, phase) (phases "start", "recomputed", "end") runs on the
+        host between a layer's launches, e.g. to snapshot `self.buffers`."""
         pool, st = self.pool, _dev.stream_handle()
         C, N = self.C, pool.N
         if self.record_timeline:
@@ -264,7 +278,7 @@ class SelectivePrefillEngine:
         logits, _ = run_layers(self.model, self.tokens, self.positions, self.n_ctx, self.caches,
                                reuse=self._reuse, logits_rows="last", buffers=self.buffers,
                                timer=self.timer,
-                               hook=self._hook if self.record_timeline else None)
+                               hook=self._step_hook(hook))
         if logits_out is not None:
             logits_out.copy_(logits, non_blocking=True)
         return logits

@@ -116,3 +116,19 @@ def test_fullsize_r1_equals_full_prefill(big):
                         suffix])
     want = full.step(tokens)
     assert torch.equal(got, want)
+
+
+def test_fullsize_oracle_attention_and_blend(big):
+    """Float64 oracle at full config-2 context (32,832 tokens) on layers 0, 15
+    and 31: the whole blended cache of each layer vs O.fuse_layer, attention
+    of 64 sampled query rows (incl. the first-token row) x 8 q heads vs the
+    oracle attention over that cache.  bf16 mode: <= 2e-2 normwise."""
+    from fullsize_oracle import check_request
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    ct, m, toks, chunks, ranks, suffix = big
+    eng = SelectivePrefillEngine(m, KvPool(chunks, ranks, "hbm"), R, S)
+    errs = check_request(eng, chunks, suffix, (0, 15, 31))
+    print("cfg2 oracle errors", errs)
+    # reused K rows are one bf16 rounding of the float64 rotation
+    assert all(e["blend_k_reused"] <= 2.0 ** -8 for e in errs.values()), errs

@@ -77,3 +77,18 @@ def test_cfg3_r1_equals_full_prefill(big3):
     tokens = torch.cat([torch.as_tensor(np.concatenate(toks).astype(np.int32), device="cuda"),
                         suffix])
     assert torch.equal(got, full.step(tokens))
+
+
+def test_cfg3_oracle_attention_and_blend_pinned(big3):
+    """Float64 oracle at full config-3 context (65,600 tokens), pool in pinned
+    host memory (the sparse PCIe path): layers 0, 15, 31 blended caches vs
+    O.fuse_layer and 64 sampled attention rows x 8 q heads vs the oracle."""
+    from fullsize_oracle import check_request
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    ct, m, toks, chunks, ranks, suffix = big3
+    eng = SelectivePrefillEngine(m, KvPool(chunks, ranks, "pinned"), R, S)
+    errs = check_request(eng, chunks, suffix, (0, 15, 31), seed=3)
+    print("cfg3 oracle errors", errs)
+    del eng
+    torch.cuda.empty_cache()
