@@ -123,7 +123,12 @@ def load(path: Path | str | None = None):
         except OSError as e:
             raise NativeLibraryMissing(f"cannot load {p}: {e}") from e
         for name, (res, args) in _SIGS.items():
-            fn = getattr(lib, name)
+            try:
+                fn = getattr(lib, name)
+            except AttributeError:
+                if path is None:  # the in-tree library must export everything
+                    raise
+                continue          # an older build loaded for an A/B comparison
             fn.restype = res
             fn.argtypes = args
         if path is None:

@@ -152,8 +152,12 @@ inline int64_t decode_keys(int64_t n_ctx, int64_t splits) {
 // 16-byte vectors along the head dim: D/VE chunks must tile the 128 threads
 inline bool decode_ok(int64_t A, int64_t Hq, int64_t Hkv, int64_t D, int dtype,
                       const float* probs) {
-  const char* e = getenv("CT_ATT_DECODE");  // CT_ATT_DECODE=0: the full kernels at tiny A
-  if (probs || (e && atoi(e) == 0) || A * (Hq / Hkv) > DEC_MAXR) return false;
+  // CT_ATT_DECODE=0: the full kernels at tiny A (read once)
+  static const bool off = [] {
+    const char* e = getenv("CT_ATT_DECODE");
+    return e && atoi(e) == 0;
+  }();
+  if (probs || off || A * (Hq / Hkv) > DEC_MAXR) return false;
   const int64_t ve = dtype == CT_BF16 ? 8 : 4;
   return D % ve == 0 && DEC_THREADS % (D / ve) == 0;
 }
@@ -394,7 +398,8 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
                  int64_t cache_row_stride, double scale, void* out, int out_dtype,
                  void* workspace, size_t workspace_bytes, cudaStream_t st);
 size_t attention_tc_workspace(int64_t A, int64_t Hq, int64_t n_ctx, int64_t Hkv, int64_t D);
-bool tc_enabled();
+bool tc_supported(const void* q, const void* k_cache, const void* v_cache, int64_t Hq,
+                  int64_t Hkv, int64_t D, int64_t cache_row_stride);
 
 }  // namespace ct
 
@@ -439,7 +444,10 @@ extern "C" int ct_selective_attention(const void* q, const int32_t* q_pos, int64
                                                   D, cache_row_stride, scale, out, workspace,
                                                   workspace_bytes, st);
   }
-  if (tc_enabled() && dtype == CT_BF16 && !probs && D == 128)
+  // bf16 without a probability record: the tcgen05 kernel whenever its
+  // preconditions hold (D = 128, GQA group | 128, 16-B aligned), else SIMT
+  if (dtype == CT_BF16 && !probs &&
+      tc_supported(q, k_cache, v_cache, Hq, Hkv, D, cache_row_stride))
     return attention_tc(q, q_pos, A, Hq, k_cache, v_cache, n_ctx, Hkv, D, cache_row_stride, scale,
                         out, out_dtype, workspace, workspace_bytes, st);
   const size_t smem = (size_t)(AT_QB * D + 2 * AT_TK * (D + 1)) * sizeof(float);

@@ -6,60 +6,45 @@
 //
 // Tile = 128 TMEM lanes = (128/G queries) x (G q-heads of one kv-head), so a
 // K/V tile staged once serves the whole GQA group.  Per 128-key block:
-//   S = Q K^T      tcgen05.mma  M128 N128 K16 x8, A=Q smem, B=K smem -> TMEM
+//   S = Q K^T      tcgen05.mma  M128 N128 K16 x8, A = Q smem, B = K smem -> TMEM
 //   softmax        one thread per row: tcgen05.ld S row, mask by position,
-//                  exp2, lazy max (rescale O only when the max grows > 2^8),
-//                  P (bf16) written swizzled to smem
-//   O += P V       tcgen05.mma  M128 N128 K16 x8, A=P smem, B=V smem (MN-major)
-// Warp roles: warps 0-7 softmax/epilogue (two warps per TMEM lane quarter,
-// each owning half of the key columns), warp 8 TMA producer, warp 9 MMA
-// issuer (+TMEM alloc).  S is double buffered in TMEM,
-// P double buffered in smem, K/V flow through a 3-slot TMA ring.
+//                  exp2 against a lazily rescaled running max, P (bf16) back
+//                  into TMEM over S
+//   O += P V       tcgen05.mma  M128 N128 K16 x8, A = P TMEM, B = V smem (MN-major)
+// Warp roles: warps 0-7 softmax/epilogue (4 per tile of a ping-pong pair),
+// warp 8 TMA producer (5-slot K/V ring + Q), warp 9 MMA issuer (+ TMEM alloc).
+// Timing-probe and CTA-pair variants measured in round 1 are not built into
+// the product library (profiles/round1_attention_variants.md; git history).
 #include "common.cuh"
 
 #include <cuda.h>
+#include <algorithm>
 #include <type_traits>
 #include <cudaTypedefs.h>
-
-// The timing-probe schedules (SCHED 3/4) end the softmax loop body with
-// `continue`, which makes the rest of the body unreachable in those
-// instantiations only.
-#pragma nv_diag_suppress 128
 
 namespace ct {
 
 namespace tc {
 
+// Diagnostic timeline (tools/build_trace.sh builds a separate library with
+// CT_ATT_TRACE): SM clock at softmax start / end and MMA PV / S issue of the
+// first unit of CTA 0, per tile and block.  Compiled out of the product.
+#ifdef CT_ATT_TRACE
+__device__ unsigned long long g_trace[14][2][512];
+#define CT_TRACE(ev_, t_, j_, cond_) \
+  if ((cond_) && blockIdx.x == 0 && (j_) < 512) g_trace[ev_][t_][j_] = clock64();
+#else
+#define CT_TRACE(ev_, t_, j_, cond_)
+#endif
+
 constexpr int TILE_M = 128;   // TMEM lanes / MMA M
 constexpr int BLK_N = 128;    // keys per block
 constexpr int HD = 128;       // head dim
 constexpr int KV_SLOTS = 5;
-constexpr int MAX_SPLIT = 4;         // softmax threads per tile row (key-column split)
-constexpr int NSB = 3;               // S/P TMEM buffers
 constexpr int ATOM_BYTES = 128 * 64 * 2;      // [128 rows][64 bf16] swizzle-128B half tile
 constexpr int TILE_BYTES = 2 * ATOM_BYTES;    // 32 KiB: 128 rows x 128 bf16
 constexpr float LAZY_THRESH = 8.0f;           // log2 units
 
-// CTAS = 1: one CTA owns a 128-row tile and stages whole K/V tiles (32 KiB).
-// CTAS = 2: a CTA pair (cluster of 2, tcgen05 cta_group::2, MMA M = 256)
-// owns two 128-row tiles; each CTA stages HALF of every K tile (64 keys) and
-// half of every V tile (64 head-dim columns), 16 KiB per slot, so per SM the
-// K/V bytes from L2 and the MMA operand reads from shared memory halve.
-template <int CTAS>
-struct Smem {
-  static constexpr int SLOT_BYTES = TILE_BYTES / CTAS;
-  static constexpr int SLOTS = CTAS == 1 ? KV_SLOTS : 2 * KV_SLOTS;
-  // offsets from the 1024-aligned base
-  static constexpr int Q = 0;
-  static constexpr int KV = Q + TILE_BYTES;
-  static constexpr int BAR = KV + SLOTS * SLOT_BYTES;
-  // q + KV full/empty + per S/P buffer (S full, P full, PV done); the
-  // exchange area must not overlap the last barrier
-  static constexpr int NBAR = 1 + 2 * SLOTS + 3 * 3;
-  static constexpr int XCH = BAR + NBAR * 8;  // [3][MAX_SPLIT][128] f32 max/sum exchange
-  static constexpr int TMEM_PTR = XCH + 3 * MAX_SPLIT * 128 * 4;
-  static constexpr int TOTAL = TMEM_PTR + 16;
-};
 
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
@@ -92,94 +77,6 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
       "l"(map), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
-}
-// 2-SM TMA: bytes land in this CTA's smem, completion counts on the LEADER's
-// mbarrier (same offset, peer bit cleared).
-__device__ __forceinline__ void tma_load_3d_2sm(uint32_t dst, const CUtensorMap* map, uint32_t bar,
-                                                int c0, int c1, int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
-      "l"(map), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-// shared::cluster address of the same smem offset in CTA `rank`
-__device__ __forceinline__ uint32_t mapa_rank(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint32_t bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "LAB_WAITC:\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
-      "@P1 bra DONEC;\n\t"
-      "bra LAB_WAITC;\n\t"
-      "DONEC:\n\t}" ::"r"(bar),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::
-                   : "memory");
-}
-template <int CTAS>
-__device__ __forceinline__ void tc_commit_t(uint32_t bar) {
-  if constexpr (CTAS == 1) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], m;\n\t}" ::"r"(bar)
-        : "memory");
-  }
-}
-template <int CTAS>
-__device__ __forceinline__ void tc_mma_t(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                         uint32_t idesc, uint32_t accum) {
-  if constexpr (CTAS == 1) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-  }
-}
-template <int CTAS>
-__device__ __forceinline__ void tc_mma_ts_t(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accum) {
-  if constexpr (CTAS == 1) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-  } else {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
-        : "memory");
-  }
 }
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -328,46 +225,6 @@ __device__ __forceinline__ void exp2_poly2(uint64_t x2, uint32_t& o0, uint32_t& 
   o0 = (uint32_t)pp + ((uint32_t)t << 23);
   o1 = (uint32_t)(pp >> 32) + ((uint32_t)(t >> 32) << 23);
 }
-// Which of a thread's 8 chunks of 8 scores take the FMA-pipe polynomial
-// instead of MUFU.ex2 (template parameter; 0 = all MUFU).
-
-// p = 2^(s*scale - m) for the thread's HALF scores: packed FFMA2 for the
-// argument, MUFU.ex2 or the polynomial per chunk (compile-time POLY), FADD2
-// row-sum accumulators, bf16x2 packing for the TMEM P store.
-__device__ __forceinline__ uint32_t pack_bf16(float a, float b);
-
-template <int HALF, uint32_t POLY>
-__device__ __forceinline__ void softmax_chunks(const uint32_t* r, uint64_t sc2, uint64_t nm2,
-                                               uint64_t* acc2, uint32_t* pk) {
-#pragma unroll
-  for (int ch = 0; ch < HALF / 8; ++ch) {
-    uint64_t x2[4];
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      x2[t] = ffma2(pk2(__uint_as_float(r[ch * 8 + 2 * t]), __uint_as_float(r[ch * 8 + 2 * t + 1])),
-                    sc2, nm2);
-    uint32_t e[8];
-    if (((POLY >> (ch & 31)) & 1) != 0) {  // folds per unrolled chunk
-#pragma unroll
-      for (int t = 0; t < 4; ++t) exp2_poly2(x2[t], e[2 * t], e[2 * t + 1]);
-    } else {
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        float x0, x1;
-        upk2(x2[t], x0, x1);
-        e[2 * t] = __float_as_uint(ex2(x0));
-        e[2 * t + 1] = __float_as_uint(ex2(x1));
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e[2 * t] | ((uint64_t)e[2 * t + 1] << 32));
-#pragma unroll
-    for (int t = 0; t < 4; ++t)
-      pk[ch * 4 + t] = pack_bf16(__uint_as_float(e[2 * t]), __uint_as_float(e[2 * t + 1]));
-  }
-}
-
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -384,496 +241,142 @@ struct Params {
   float lazy_thresh;
 };
 
-template <int NSPLIT, uint32_t POLY_MASK, int EXPT = 0, int CTAS = 1>
-__global__ void __launch_bounds__(32 * (4 * NSPLIT + 2), 1)
-attention_tc_kernel(const __grid_constant__ CUtensorMap map_q,
-                    const __grid_constant__ CUtensorMap map_k,
-                    const __grid_constant__ CUtensorMap map_v, const Params p) {
-  constexpr int SOFTMAX_WARPS = 4 * NSPLIT;
-  constexpr int TMA_WARP = SOFTMAX_WARPS, MMA_WARP = SOFTMAX_WARPS + 1;
-  constexpr int HALF = BLK_N / NSPLIT;  // key columns per softmax thread
-  constexpr int NSM = 32 * SOFTMAX_WARPS;
-  using SM = Smem<CTAS>;
-  constexpr int NSLOT = SM::SLOTS;
-  constexpr int SLOT = SM::SLOT_BYTES;
-  extern __shared__ uint8_t smem_raw[];
-  const uint32_t raw = su32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
-  uint8_t* gbase = smem_raw + (base - raw);
-  const uint32_t sQ = base + SM::Q, sKV = base + SM::KV;
-  const uint32_t bar0 = base + SM::BAR;
-  const uint32_t crank = CTAS == 2 ? cluster_rank() : 0u;
-  const bool leader = crank == 0;
-  // barriers
-  const uint32_t bar_q = bar0 + 0 * 8;
-  auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };
-  auto bar_empty = [&](int s) { return bar0 + (1 + NSLOT + s) * 8; };
-  constexpr int B2 = 1 + 2 * NSLOT;
-  // per S/P TMEM buffer (3): S landed, P written, PV (the reader of P) done
-  auto bar_sfull = [&](int b) { return bar0 + (B2 + b) * 8; };
-  auto bar_pfull = [&](int b) { return bar0 + (B2 + 3 + b) * 8; };
-  auto bar_pvdone = [&](int b) { return bar0 + (B2 + 6 + b) * 8; };
-  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + SM::TMEM_PTR);
-
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // longest tiles first: high query blocks (largest positions) get low block
-  // ids.  A CTA pair takes two adjacent query blocks of one kv head.
-  const int tile = blockIdx.x / CTAS;
-  const int n_units = (p.n_qblocks + CTAS - 1) / CTAS;
-  const int qb0 = (n_units - 1 - (tile / p.Hkv)) * CTAS;
-  const int qb = qb0 + (int)crank;
-  const int g = tile % p.Hkv;
-  const int a0 = qb * p.QB;
-
-  // key range: the pair shares every K/V block, so both use the pair's max
-  int maxpos = 0;
-  for (int i = 0; i < CTAS * p.QB; ++i) {
-    const int a = qb0 * p.QB + i;
-    if (a < p.A) maxpos = max(maxpos, __ldg(p.qpos + a));
-  }
-  maxpos = min(maxpos, p.n_ctx - 1);
-  const int nb = maxpos / BLK_N + 1;
-
-  if (threadIdx.x == 0) {
-    // full / q: the leader's copies count one arrive per CTA of the pair (the
-    // leader's carries expect_tx for both CTAs' bytes); pfull: one elected
-    // arrive per softmax warp of every CTA of the pair
-    mbar_init(bar_q, CTAS);
-    for (int s = 0; s < NSLOT; ++s) {
-      mbar_init(bar_full(s), CTAS);
-      mbar_init(bar_empty(s), 1);
-    }
-    for (int b = 0; b < NSB; ++b) {
-      mbar_init(bar_sfull(b), 1);
-      mbar_init(bar_pfull(b), (EXPT == 3 ? 1 : CTAS) * SOFTMAX_WARPS);
-      mbar_init(bar_pvdone(b), 1);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == MMA_WARP) {
-    if constexpr (CTAS == 1) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       su32(tmem_ptr)),
-                   "r"(512)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
-    } else {
-      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                       su32(tmem_ptr)),
-                   "r"(512)
-                   : "memory");
-      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
-    }
-  }
-  tc_fence_before();
-  if constexpr (CTAS == 2) cluster_sync_all();  // peer barriers initialised before any signal
-  else __syncthreads();
-  tc_fence_after();
-  // leader-side copy of a barrier (remote for the peer CTA)
-  auto to_leader = [&](uint32_t bar) { return CTAS == 2 ? mapa_rank(bar, 0) : bar; };
-  auto arrive_tx = [&](uint32_t bar, uint32_t bytes) {
-    if (leader) mbar_expect_tx(bar, bytes * CTAS);
-    else mbar_arrive_cluster(to_leader(bar));
-  };
-  const uint32_t tbase = *tmem_ptr;
-  // TMEM: three S buffers (128 fp32 columns each) + O (128).  P_j (bf16x2,
-  // 64 columns) overwrites the first half of S_j's buffer once the softmax
-  // has read S_j; the PV MMA reads it as its TMEM A operand, so P never
-  // touches shared memory.  Three buffers let S run two blocks ahead.
-  auto tS = [&](int b) { return tbase + (uint32_t)(b * 128); };
-  const uint32_t tO = tbase + 384;
-
-  if (warp == TMA_WARP) {
-    // ------------------------------------------------------------ TMA producer
-    if (lane == 0) {
-      auto tma = [&](uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2) {
-        if constexpr (CTAS == 1) tma_load_3d(dst, m, bar, c0, c1, c2);
-        else tma_load_3d_2sm(dst, m, bar, c0, c1, c2);
-      };
-      arrive_tx(bar_q, TILE_BYTES);
-      tma(sQ, &map_q, bar_q, 0, g * p.G, a0);
-      tma(sQ + ATOM_BYTES, &map_q, bar_q, 64, g * p.G, a0);
-      int slot = 0;
-      uint32_t phase = 0;
-      // K_j: CTAS=1 the whole [128 keys][128 d] tile (two 64-d swizzle atoms);
-      // CTAS=2 keys [64r, 64r+64) of the block (MMA N half r), both d atoms.
-      int nloads = 0;
-      auto load_k = [&](int j) {
-        mbar_wait(bar_empty(slot), phase ^ 1);
-        const uint32_t dst = sKV + slot * SLOT;
-        if (EXPT == 4 && ++nloads > NSLOT) {  // probe: slots keep stale data
-          if (leader) mbar_arrive(bar_full(slot));
-          else mbar_arrive_cluster(to_leader(bar_full(slot)));
-          if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-          return;
-        }
-        arrive_tx(bar_full(slot), SLOT);
-        const int key0 = j * BLK_N + (int)crank * (BLK_N / CTAS);
-        tma(dst, &map_k, bar_full(slot), 0, g, key0);
-        tma(dst + SLOT / 2, &map_k, bar_full(slot), 64, g, key0);
-        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-      };
-      // V_j: CTAS=1 both 64-d atoms; CTAS=2 the d atom r (MMA N half r).
-      auto load_v = [&](int j) {
-        mbar_wait(bar_empty(slot), phase ^ 1);
-        const uint32_t dst = sKV + slot * SLOT;
-        if (EXPT == 4 && ++nloads > NSLOT) {
-          if (leader) mbar_arrive(bar_full(slot));
-          else mbar_arrive_cluster(to_leader(bar_full(slot)));
-          if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-          return;
-        }
-        arrive_tx(bar_full(slot), SLOT);
-        if constexpr (CTAS == 1) {
-          tma(dst, &map_v, bar_full(slot), 0, g, j * BLK_N);
-          tma(dst + ATOM_BYTES, &map_v, bar_full(slot), 64, g, j * BLK_N);
-        } else {
-          tma(dst, &map_v, bar_full(slot), 64 * (int)crank, g, j * BLK_N);
-        }
-        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-      };
-      // same order the MMA warp consumes: K0, K1, K2, V0, K3, V1, K4, ...
-      for (int j = 0; j < NSB && j < nb; ++j) load_k(j);
-      for (int j = 0; j < nb; ++j) {
-        load_v(j);
-        if (j + NSB < nb) load_k(j + NSB);
-      }
-    }
-  } else if (warp == MMA_WARP) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0 && leader) {
-      constexpr uint32_t IDESC_S = idesc_bf16(false, TILE_M * CTAS);
-      constexpr uint32_t IDESC_O = idesc_bf16(true, TILE_M * CTAS);
-      constexpr int KATOM = SLOT / 2;  // bytes of one 64-d K atom in a slot
-      mbar_wait(bar_q, 0);
-      tc_fence_after();
-      int slot = 0;
-      uint32_t phase = 0;
-      // S_j goes into TMEM buffer j%3, which last held P_{j-3}.  S_j is issued
-      // right after PV_{j-3} (its reader) by this thread, and tcgen05.mma ops
-      // from one thread execute in issue order, so no wait is needed: two S
-      // blocks stay queued ahead of every PV while the softmax works.
-      auto issue_s = [&](int j) {
-        const int b = j % NSB;
-        mbar_wait(bar_full(slot), phase);
-        tc_fence_after();
-        const uint32_t k_tile = sKV + slot * SLOT;
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t koff = (kk & 3) * 32;
-          tc_mma_t<CTAS>(tS(b), sdesc(sQ + (kk >> 2) * ATOM_BYTES + koff, 16, 1024),
-                         sdesc(k_tile + (kk >> 2) * KATOM + koff, 16, 1024), IDESC_S, kk > 0);
-        }
-        tc_commit_t<CTAS>(bar_empty(slot));
-        tc_commit_t<CTAS>(bar_sfull(b));
-        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-      };
-      for (int j = 0; j < NSB && j < nb; ++j) issue_s(j);
-      for (int j = 0; j < nb; ++j) {
-        // O += P_j V_j
-        const int b = j % NSB;
-        if constexpr (CTAS == 2) mbar_wait_cluster(bar_pfull(b), (j / NSB) & 1);
-        else mbar_wait(bar_pfull(b), (j / NSB) & 1);
-        mbar_wait(bar_full(slot), phase);
-        tc_fence_after();
-        const uint32_t v_tile = sKV + slot * SLOT;
-#pragma unroll
-        for (int kk = 0; kk < BLK_N / 16; ++kk) {
-          // A = P from TMEM (16 keys = 8 packed columns); B = V, MN-major,
-          // K-step of 16 keys = 2 x 1024 B core-matrix groups
-          tc_mma_ts_t<CTAS>(tO, tS(b) + kk * 8, sdesc(v_tile + kk * 2048, ATOM_BYTES, 1024),
-                            IDESC_O, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc_commit_t<CTAS>(bar_empty(slot));
-        tc_commit_t<CTAS>(bar_pvdone(b));
-        if (++slot == NSLOT) { slot = 0; phase ^= 1; }
-        if (j + NSB < nb) issue_s(j + NSB);
-      }
-    }
-  } else {
-    // ------------------------------------------------------------ softmax
-    // 8 warps: warp w owns TMEM lanes 32*(w%4).. (tile rows) and the column
-    // half hf = w/4 (keys 64*hf .. +63 of each block, O columns likewise), so
-    // every SMSP runs two softmax warps.  The two halves of a row agree on the
-    // running max through a double-buffered smem exchange + named barrier.
-    const int hf = warp >> 2;
-    const int m = (warp & 3) * 32 + lane;  // TMEM lane / tile row
-    const int qi = m / p.G, hj = m % p.G;
-    const int a = a0 + qi;
-    const bool valid = a < p.A;
-    const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
-    const uint32_t lane_off = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF);
-    const uint32_t lane_off_p = ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(hf * HALF / 2);
-    float* xch = reinterpret_cast<float*>(gbase + SM::XCH);  // [3][2][128]
-    float m_used = -INFINITY, l = 0.f;
-    uint32_t r[HALF];
-    for (int j = 0; j < nb; ++j) {
-      const int b = j % NSB;
-      mbar_wait(bar_sfull(b), (j / NSB) & 1);
-      // lanes leave the try_wait spin independently: reconverge before the
-      // warp-collective (.sync.aligned) tcgen05.ld
-      __syncwarp();
-      tc_fence_after();
-      if constexpr (EXPT == 2 || EXPT == 3 || EXPT == 4) {  // profiling aid: no softmax
-        tc_fence_before();
-        __syncwarp();
-        if (EXPT == 3 && !leader) continue;  // EXPT 3: leader does not wait for the peer
-        if (lane == 0) {
-          if constexpr (CTAS == 2) mbar_arrive_cluster(to_leader(bar_pfull(b)));
-          else mbar_arrive(bar_pfull(b));
-        }
-        continue;
-      }
-      if constexpr (EXPT == 1) {  // profiling aid: TMEM S load + P store only
-#pragma unroll
-        for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS(b) + lane_off + c * 32, r + c * 32);
-#pragma unroll
-        for (int c = 0; c < HALF / 32; ++c) tmem_wait_ld32(r + c * 32);
-        uint32_t pk[HALF / 2];
-#pragma unroll
-        for (int c = 0; c < HALF / 2; ++c) pk[c] = r[2 * c] ^ r[2 * c + 1];
-        asm volatile("bar.sync 1, %0;" ::"n"(NSM) : "memory");
-        __syncwarp();
-#pragma unroll
-        for (int c = 0; c < HALF / 64; ++c) tmem_st32(tS(b) + lane_off_p + c * 32, pk + c * 32);
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) {
-          if constexpr (CTAS == 2) mbar_arrive_cluster(to_leader(bar_pfull(b)));
-          else mbar_arrive(bar_pfull(b));
-        }
-        continue;
-      }
-#pragma unroll
-      for (int c = 0; c < HALF / 32; ++c) tmem_ld32(tS(b) + lane_off + c * 32, r + c * 32);
-#pragma unroll
-      for (int c = 0; c < HALF / 32; ++c) tmem_wait_ld32(r + c * 32);
-      const int kbase = j * BLK_N + hf * HALF;
-      const bool need_mask = kbase + HALF - 1 > pos;
-      if (need_mask) {
-#pragma unroll
-        for (int c = 0; c < HALF; ++c)
-          if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
-      }
-      // row max of the raw scores (scale > 0 commutes with max)
-      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < HALF; c += 8) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
-      }
-      const float pm = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3]));
-      float* xb = xch + (j & 1) * (NSPLIT * 128);
-      float mrow = pm;
-      if constexpr (NSPLIT > 1) {
-        xb[hf * 128 + m] = pm;
-        // also orders every half's S_j reads before any half's P_j writes
-        // (P_j aliases the first half of S_j's TMEM columns)
-        tc_fence_before();
-        asm volatile("bar.sync 1, %0;" ::"n"(NSM) : "memory");
-        tc_fence_after();
-#pragma unroll
-        for (int o = 1; o < NSPLIT; ++o) mrow = fmaxf(mrow, xb[((hf + o) % NSPLIT) * 128 + m]);
-      }
-      const float mx = mrow * p.scale_log2;
-      const float m_new = fmaxf(m_used, mx);
-      const bool grow = m_new > m_used + p.lazy_thresh;
-      // warp-uniform decision (tcgen05.ld/st are .sync.aligned).  P_j is built
-      // with the new max first; the O rescale (which must wait for PV_{j-1})
-      // runs after P_j is in smem so it overlaps PV_{j-1} instead of stalling.
-      const bool any_grow = __any_sync(0xffffffffu, grow);
-      const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
-      if (grow) m_used = m_new;
-      // P_j half-row into smem buffer b: atom hf (K-major SW128, chunk c^(m&7))
-      uint32_t pk[HALF / 2];  // packed bf16x2 P for this thread's key columns
-      const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
-      const uint64_t nm2 = pk2(-m_used, -m_used);
-      uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
-      // masked (diagonal) blocks take the all-MUFU path: -inf must give 0
-      if (need_mask)
-        softmax_chunks<HALF, 0u>(r, sc2, nm2, acc2, pk);
-      else
-        softmax_chunks<HALF, POLY_MASK>(r, sc2, nm2, acc2, pk);
-      {
-        float s0, s1, s2, s3;
-        upk2(acc2[0], s0, s1);
-        upk2(acc2[1], s2, s3);
-        l = l * corr + ((s0 + s1) + (s2 + s3));  // partial row sum over this half
-      }
-      // P_j -> TMEM columns [hf*HALF/2, +HALF/2) of P buffer b (lane m)
-      __syncwarp();
-#pragma unroll
-      for (int c = 0; c < HALF / 64; ++c) tmem_st32(tS(b) + lane_off_p + c * 32, pk + c * 32);
-      if constexpr (HALF / 2 < 32) tmem_st16(tS(b) + lane_off_p, pk);
-      tmem_wait_st();
-      if (any_grow && j > 0) {
-        // O[:, half] *= corr once PV_{j-1} has landed.  The parity test on
-        // buffer (j-1)%3's barrier cannot alias: its previous phase (PV_{j-4})
-        // completed before S_j was issued into buffer j%3 (in-order pipe).
-        mbar_wait(bar_pvdone((j - 1) % NSB), ((j - 1) / NSB) & 1);
-        __syncwarp();  // reconverge before tcgen05.ld/st (.sync.aligned)
-        tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < HALF / 32; ++c) {
-          uint32_t o[32];
-          tmem_ld32(tO + lane_off + c * 32, o);
-          tmem_wait_ld32(o);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-          tmem_st32(tO + lane_off + c * 32, o);
-        }
-        tmem_wait_st();
-      }
-      tc_fence_before();
-      __syncwarp();  // every lane's P store + O rescale precede the warp's arrive
-      if (lane == 0) {
-          if constexpr (CTAS == 2) mbar_arrive_cluster(to_leader(bar_pfull(b)));
-          else mbar_arrive(bar_pfull(b));
-        }
-    }
-    // epilogue: combine the two partial row sums, O[:, half] / l -> global
-    if constexpr (NSPLIT > 1) {
-      float* xl = xch + 2 * NSPLIT * 128;
-      xl[hf * 128 + m] = l;
-      asm volatile("bar.sync 1, %0;" ::"n"(NSM) : "memory");
-      float lt = 0.f;
-#pragma unroll
-      for (int o = 0; o < NSPLIT; ++o) lt += xl[o * 128 + m];
-      l = lt;
-    }
-    mbar_wait(bar_pvdone((nb - 1) % NSB), ((nb - 1) / NSB) & 1);  // PV_{nb-1} done
-    __syncwarp();
-    tc_fence_after();
-    const float inv = valid ? 1.f / l : 0.f;
-    const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD + hf * HALF;
-#pragma unroll 1
-    for (int c = 0; c < HALF / 32; ++c) {
-      uint32_t o[32];
-      tmem_ld32(tO + lane_off + c * 32, o);
-      tmem_wait_ld32(o);
-      if (valid) {
-        if (p.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(p.out_f32 + orow + c * 32);
-#pragma unroll
-          for (int e = 0; e < 8; ++e)
-            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(p.out + orow + c * 32);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
-            v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
-            v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
-            v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
-            dst[e] = v;
-          }
-        }
-      }
-    }
-  }
-  tc_fence_before();
-  if constexpr (CTAS == 2) cluster_sync_all();  // both CTAs done with TMEM and barriers
-  else __syncthreads();
-  if (warp == MMA_WARP) {
-    tc_fence_after();
-    if constexpr (CTAS == 1)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
-                   : "memory");
-    else
-      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tbase), "r"(512)
-                   : "memory");
-  }
-}
 
 // ---------------------------------------------------------------------------
-// Ping-pong kernel: two 128-row query tiles (X = 0, 1: adjacent query blocks
-// of one kv head) per CTA share every K/V tile.  TMEM = S_0 | S_1 | O_0 | O_1
-// (128 columns each; P_X aliases the first half of S_X).  One softmax thread
-// per tile row (warps 0-3 tile 0, warps 4-7 tile 1, so every SMSP runs one
-// warp of each tile), and the MMA order
+// Persistent ping-pong kernel.  A work unit is two adjacent 128-row query
+// tiles (X = 0, 1) of one kv head; they share every K/V tile.  One CTA per SM
+// walks its units (longest first, snake order over the CTAs) with ONE TMEM
+// allocation and one barrier set for its lifetime; the TMA producer runs into
+// the next unit's Q and K/V while the softmax warps finish the current
+// unit's epilogue.  TMEM = S_0 | S_1 | O_0 | O_1 (128 columns each; P_X, bf16,
+// overwrites the first half of S_X and is the A operand of the PV MMA).  One
+// softmax thread per tile row (warps 0-3 tile 0, warps 4-7 tile 1: every SMSP
+// runs one warp of each tile), MMA order
 //     S_0(0) S_1(0) | PV_0(j) S_0(j+1) PV_1(j) S_1(j+1) | ...
-// keeps one tile's MMAs in the pipe while the other tile's softmax runs, so
-// the two softmax warps of an SMSP are out of phase and the exp2 (MUFU) work
-// of one overlaps the TMEM load / row max / P store of the other.  K/V bytes
-// per FLOP from L2 halve versus the single-tile kernel.
+// (S_X(j+1) overwrites P_X(j): it is issued right behind PV_X(j), the
+// tcgen05 pipe of one thread executes in order).
+//
+// Softmax per block: one thread per row reads its 128 scores from TMEM,
+// masks the diagonal block (warp-uniform branch), takes the row max, and
+// keeps a lazily rescaled running max (O and the row sum are rescaled only
+// when a row grows by more than 2^lazy_thresh).  The exp2 of the four 32-key
+// chunks runs interleaved: MUFU for most, the FMA-pipe polynomial for the
+// POLY chunks of unmasked blocks, so one warp keeps both pipes busy.
 // ---------------------------------------------------------------------------
-template <int SLOTS_ = 5>
 struct SmemPP {
-  static constexpr int SLOTS = SLOTS_;
+  static constexpr int SLOTS = KV_SLOTS;
   static constexpr int Q = 0;                        // two Q tiles
   static constexpr int KV = Q + 2 * TILE_BYTES;
   static constexpr int BAR = KV + SLOTS * TILE_BYTES;
-  // q, full[SLOTS], empty[SLOTS], per tile: sfull, pfull, pvdone
-  static constexpr int NBAR = 1 + 2 * SLOTS + 6;
-  // split-row variant: [2 parity][2 tiles][2 halves][128 rows] f32 max / sum exchange
-  static constexpr int XCH = BAR + NBAR * 8;
-  static constexpr int XCH_BYTES = SLOTS_ < 5 ? 2 * 2 * 2 * 128 * 4 : 0;
-  static constexpr int TMEM_PTR = XCH + XCH_BYTES;
+  // q full, q empty, full[SLOTS], empty[SLOTS], per tile: sfull, pfull (two
+  // key halves), pvdone
+  static constexpr int NBAR = 2 + 2 * SLOTS + 8;
+  static constexpr int TMEM_PTR = BAR + NBAR * 8;
   static constexpr int TOTAL = TMEM_PTR + 16;
 };
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+// Work unit `u` of the longest-first order: query-block pair and kv head.
+struct Unit {
+  int qb0, g, nb, maxpos;
+};
+__device__ __forceinline__ Unit unit_of(const Params& p, int u) {
+  const int n_pairs = (p.n_qblocks + 1) / 2;
+  Unit w;
+  w.qb0 = (n_pairs - 1 - u / p.Hkv) * 2;
+  w.g = u % p.Hkv;
+  int maxpos = 0;
+  for (int i = 0; i < 2 * p.QB; ++i) {
+    const int a = w.qb0 * p.QB + i;
+    if (a < p.A) maxpos = max(maxpos, __ldg(p.qpos + a));
+  }
+  w.maxpos = min(maxpos, p.n_ctx - 1);
+  w.nb = w.maxpos / BLK_N + 1;
+  return w;
+}
+// i-th unit of CTA c: rounds of gridDim.x units, alternate rounds reversed
+__device__ __forceinline__ int unit_index(int i, int c, int grid) {
+  return i * grid + ((i & 1) ? grid - 1 - c : c);
 }
 
-// SPLIT = 2: two softmax threads per tile row (16 softmax warps; warp
-// x*8 + h*4 + q owns TMEM lane quarter q of tile x and key columns
-// [64h, 64h+64) of every block), halving the per-tile S -> softmax -> PV
-// latency; the two halves agree on the running max through a 64-thread named
-// barrier per lane quarter, P of half h lands in TMEM columns [64h, 64h+32) of
-// S, and each half rescales / stores its 64 O columns.  Needs the exchange
-// area, so it runs with 4 K/V slots.
-template <uint32_t POLY_MASK, int SCHED = 1, int SPLIT = 1, int SLOTS = 5>
-__global__ void __launch_bounds__(32 * (8 * SPLIT + 2), 1)
+// P of 64 keys of a row (two 32-key chunks): element pair t of chunk c ->
+// 2^(s*scale - m) via MUFU, or via the FMA-pipe polynomial when bit c of POLY
+// is set; bf16x2 into pk[16c + t]; row sums per chunk (two FADD2 lanes
+// each), added in chunk order.
+template <uint32_t POLY>
+__device__ __forceinline__ float p_half(const uint32_t* r, uint64_t sc2, uint64_t nm2,
+                                        uint32_t* pk) {
+  uint64_t acc[2][2];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) acc[c][0] = acc[c][1] = pk2(0.f, 0.f);
+#pragma unroll
+  for (int t = 0; t < 16; ++t) {
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      const int i = 32 * c + 2 * t;
+      const uint64_t a2 = ffma2(pk2(__uint_as_float(r[i]), __uint_as_float(r[i + 1])), sc2, nm2);
+      uint32_t e0, e1;
+      if ((POLY >> c) & 1) {
+        exp2_poly2(a2, e0, e1);
+      } else {
+        float a, b;
+        upk2(a2, a, b);
+        e0 = __float_as_uint(ex2(a));
+        e1 = __float_as_uint(ex2(b));
+      }
+      acc[c][t & 1] = fadd2(acc[c][t & 1], (uint64_t)e0 | ((uint64_t)e1 << 32));
+      pk[16 * c + t] = pack_bf16(__uint_as_float(e0), __uint_as_float(e1));
+    }
+  }
+  float sum = 0.f;
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float s0, s1, s2, s3;
+    upk2(acc[c][0], s0, s1);
+    upk2(acc[c][1], s2, s3);
+    sum += (s0 + s1) + (s2 + s3);
+  }
+  return sum;
+}
+
+template <uint32_t POLY_MASK>
+__global__ void __launch_bounds__(32 * 10, 1)
 attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
                     const __grid_constant__ CUtensorMap map_k,
                     const __grid_constant__ CUtensorMap map_v, const Params p) {
-  using SM = SmemPP<SLOTS>;
-  constexpr int TMA_WARP = 8 * SPLIT, MMA_WARP = 8 * SPLIT + 1;
+  using SM = SmemPP;
+  constexpr int TMA_WARP = 8, MMA_WARP = 9;
   constexpr int NSLOT = SM::SLOTS;
-  static_assert(SPLIT == 1 || (SPLIT == 2 && SM::XCH_BYTES > 0), "split rows need the exchange area");
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t sQ = base + SM::Q, sKV = base + SM::KV;
   const uint32_t bar0 = base + SM::BAR;
-  const uint32_t bar_q = bar0;
-  auto bar_full = [&](int s) { return bar0 + (1 + s) * 8; };
-  auto bar_empty = [&](int s) { return bar0 + (1 + NSLOT + s) * 8; };
-  constexpr int B2 = 1 + 2 * NSLOT;
+  const uint32_t bar_q = bar0, bar_qempty = bar0 + 8;
+  auto bar_full = [&](int s) { return bar0 + (2 + s) * 8; };
+  auto bar_empty = [&](int s) { return bar0 + (2 + NSLOT + s) * 8; };
+  constexpr int B2 = 2 + 2 * NSLOT;
   auto bar_sfull = [&](int x) { return bar0 + (B2 + x) * 8; };
-  auto bar_pfull = [&](int x) { return bar0 + (B2 + 2 + x) * 8; };
-  auto bar_pvdone = [&](int x) { return bar0 + (B2 + 4 + x) * 8; };
+  // P of keys [64h, 64h+64) of tile x stored (h = 0, 1)
+  auto bar_pfull = [&](int x, int h) { return bar0 + (B2 + 2 + 2 * x + h) * 8; };
+  auto bar_pvdone = [&](int x) { return bar0 + (B2 + 6 + x) * 8; };
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(gbase + SM::TMEM_PTR);
-  float* xch = reinterpret_cast<float*>(gbase + SM::XCH);  // [parity][tile][half][row]
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // longest units first; unit = two adjacent query blocks of kv head g
-  const int n_units = (p.n_qblocks + 1) / 2;
-  const int qb0 = (n_units - 1 - (int)(blockIdx.x / p.Hkv)) * 2;
-  const int g = blockIdx.x % p.Hkv;
-  int maxpos = 0;
-  for (int i = 0; i < 2 * p.QB; ++i) {
-    const int a = qb0 * p.QB + i;
-    if (a < p.A) maxpos = max(maxpos, __ldg(p.qpos + a));
-  }
-  maxpos = min(maxpos, p.n_ctx - 1);
-  const int nb = maxpos / BLK_N + 1;
+  const int n_units = ((p.n_qblocks + 1) / 2) * p.Hkv;
+  const int grid = (int)gridDim.x, cta = (int)blockIdx.x;
 
   if (threadIdx.x == 0) {
     mbar_init(bar_q, 1);
+    mbar_init(bar_qempty, 1);
     for (int s = 0; s < NSLOT; ++s) {
       mbar_init(bar_full(s), 1);
       mbar_init(bar_empty(s), 1);
     }
     for (int x = 0; x < 2; ++x) {
       mbar_init(bar_sfull(x), 1);
-      mbar_init(bar_pfull(x), 4 * SPLIT);  // one elected arrive per softmax warp of the tile
+      mbar_init(bar_pfull(x, 0), 4);  // one elected arrive per softmax warp of the tile
+      mbar_init(bar_pfull(x, 1), 4);
       mbar_init(bar_pvdone(x), 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -895,25 +398,35 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
   if (warp == TMA_WARP) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      mbar_expect_tx(bar_q, 2 * TILE_BYTES);
-      for (int x = 0; x < 2; ++x) {
-        const int a0 = (qb0 + x) * p.QB;
-        tma_load_3d(sQ + x * TILE_BYTES, &map_q, bar_q, 0, g * p.G, a0);
-        tma_load_3d(sQ + x * TILE_BYTES + ATOM_BYTES, &map_q, bar_q, 64, g * p.G, a0);
-      }
-      int slot = 0;
+      int slot = 0, i_unit = 0;
       uint32_t phase = 0;
-      auto load = [&](const CUtensorMap* m, int j) {
+      (void)i_unit;
+      auto load = [&](const CUtensorMap* m, int g, int j, int tr) {
         mbar_wait(bar_empty(slot), phase ^ 1);
+        CT_TRACE(6, tr, j, i_unit == 0);
         const uint32_t dst = sKV + slot * TILE_BYTES;
         mbar_expect_tx(bar_full(slot), TILE_BYTES);
         tma_load_3d(dst, m, bar_full(slot), 0, g, j * BLK_N);
         tma_load_3d(dst + ATOM_BYTES, m, bar_full(slot), 64, g, j * BLK_N);
         if (++slot == NSLOT) { slot = 0; phase ^= 1; }
       };
-      for (int j = 0; j < nb; ++j) {  // consumption order: K0 V0 K1 V1 ...
-        load(&map_k, j);
-        load(&map_v, j);
+      for (int i = 0;; ++i) {
+        const int u = unit_index(i, cta, grid);
+        if (u >= n_units) break;
+        const Unit w = unit_of(p, u);
+        i_unit = i;
+        // Q of this unit once the previous unit's last S MMA has read Q
+        mbar_wait(bar_qempty, (uint32_t)((i & 1) ^ 1));
+        mbar_expect_tx(bar_q, 2 * TILE_BYTES);
+        for (int x = 0; x < 2; ++x) {
+          const int a0 = (w.qb0 + x) * p.QB;
+          tma_load_3d(sQ + x * TILE_BYTES, &map_q, bar_q, 0, w.g * p.G, a0);
+          tma_load_3d(sQ + x * TILE_BYTES + ATOM_BYTES, &map_q, bar_q, 64, w.g * p.G, a0);
+        }
+        for (int j = 0; j < w.nb; ++j) {  // consumption order: K0 V0 K1 V1 ...
+          load(&map_k, w.g, j, 0);
+          load(&map_v, w.g, j, 1);
+        }
       }
     }
   } else if (warp == MMA_WARP) {
@@ -921,247 +434,213 @@ attention_pp_kernel(const __grid_constant__ CUtensorMap map_q,
     if (lane == 0) {
       constexpr uint32_t IDESC_S = idesc_bf16(false);
       constexpr uint32_t IDESC_O = idesc_bf16(true);
-      mbar_wait(bar_q, 0);
-      tc_fence_after();
-      // K_j lives in slot (2j) % NSLOT, V_j in (2j+1) % NSLOT
-      auto slot_of = [&](int i) { return i % NSLOT; };
-      auto par_of = [&](int i) { return (uint32_t)((i / NSLOT) & 1); };
-      auto issue_s = [&](int x, int j) {
-        const int i = 2 * j, s = slot_of(i);
-        if (x == 0) {
-          mbar_wait(bar_full(s), par_of(i));
-          tc_fence_after();
-        }
-        // descriptors are linear in the (16-B unit) start address: build the
-        // tile's once and step them by the K-slice offset
-        const uint64_t qd = sdesc(sQ + x * TILE_BYTES, 16, 1024);
-        const uint64_t kd = sdesc(sKV + s * TILE_BYTES, 16, 1024);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off16 = ((kk >> 2) * ATOM_BYTES + (kk & 3) * 32) >> 4;
-          tc_mma(tS(x), qd + off16, kd + off16, IDESC_S, kk > 0);
-        }
-        if (x == 1) tc_commit(bar_empty(s));
-        tc_commit(bar_sfull(x));
-      };
-      auto issue_pv = [&](int x, int j) {
-        const int i = 2 * j + 1, s = slot_of(i);
-        mbar_wait(bar_pfull(x), (uint32_t)(j & 1));
-        if (x == 0) mbar_wait(bar_full(s), par_of(i));
+      int ring = 0;   // K/V ring position (2 per block)
+      int gb = 0;     // blocks issued so far (both tiles), for barrier parities
+      for (int i = 0;; ++i) {
+        const int u = unit_index(i, cta, grid);
+        if (u >= n_units) break;
+        const int nb = unit_of(p, u).nb;
+        mbar_wait(bar_q, (uint32_t)(i & 1));
         tc_fence_after();
-        const uint64_t vd = sdesc(sKV + s * TILE_BYTES, ATOM_BYTES, 1024);
+        auto issue_s = [&](int x, int j) {
+          const int ri = ring + 2 * j, s = ri % NSLOT;
+          if (x == 0) {
+            mbar_wait(bar_full(s), (uint32_t)((ri / NSLOT) & 1));
+            tc_fence_after();
+          }
+          const uint64_t qd = sdesc(sQ + x * TILE_BYTES, 16, 1024);
+          const uint64_t kd = sdesc(sKV + s * TILE_BYTES, 16, 1024);
 #pragma unroll
-        for (int kk = 0; kk < BLK_N / 16; ++kk) {
-          // P of keys [16kk, 16kk+16): bf16x2 columns 8kk (one softmax thread
-          // per row) or 64*(kk/4) + 8*(kk%4) (half h stores over its own S columns)
-          const uint32_t pcol = SPLIT == 1 ? kk * 8 : (kk >> 2) * 64 + (kk & 3) * 8;
-          tc_mma_ts(tO(x), tS(x) + pcol, vd + (uint64_t)(kk * 2048 / 16), IDESC_O,
-                    (j > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off16 = ((kk >> 2) * ATOM_BYTES + (kk & 3) * 32) >> 4;
+            tc_mma(tS(x), qd + off16, kd + off16, IDESC_S, kk > 0);
+          }
+          if (x == 1) {
+            tc_commit(bar_empty(s));
+            if (j == nb - 1) tc_commit(bar_qempty);  // Q fully read: next unit's Q may land
+          }
+          tc_commit(bar_sfull(x));
+          CT_TRACE(3, x, j, i == 0);
+        };
+        auto issue_pv = [&](int x, int j) {
+          const int ri = ring + 2 * j + 1, s = ri % NSLOT;
+          const uint32_t par = (uint32_t)((gb + j) & 1);
+          CT_TRACE(5, x, j, i == 0);
+          if (x == 0) mbar_wait(bar_full(s), (uint32_t)((ri / NSLOT) & 1));
+          CT_TRACE(12, x, j, i == 0);
+          const uint64_t vd = sdesc(sKV + s * TILE_BYTES, ATOM_BYTES, 1024);
+          // the first key half's PV runs while the softmax finishes the second
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(bar_pfull(x, h), par);
+            tc_fence_after();
+            if (h == 0) CT_TRACE(2, x, j, i == 0);
+#pragma unroll
+            for (int kk = 4 * h; kk < 4 * h + 4; ++kk)
+              // A = P_x: keys [16kk, 16kk+16) = bf16x2 TMEM columns [8kk, 8kk+8)
+              tc_mma_ts(tO(x), tS(x) + kk * 8, vd + (uint64_t)(kk * 2048 / 16), IDESC_O,
+                        (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          if (x == 1) tc_commit(bar_empty(s));
+          tc_commit(bar_pvdone(x));
+        };
+        issue_s(0, 0);
+        issue_s(1, 0);
+        for (int j = 0; j < nb; ++j) {
+          issue_pv(0, j);
+          if (j + 1 < nb) issue_s(0, j + 1);
+          issue_pv(1, j);
+          if (j + 1 < nb) issue_s(1, j + 1);
         }
-        if (x == 1) tc_commit(bar_empty(s));
-        tc_commit(bar_pvdone(x));
-      };
-      issue_s(0, 0);
-      issue_s(1, 0);
-      for (int j = 0; j < nb; ++j) {
-        // S_x(j+1) overwrites the columns PV_x(j) reads as P: same thread,
-        // in-order tcgen05.mma pipe, so it is issued right behind it
-        issue_pv(0, j);
-        if (j + 1 < nb) issue_s(0, j + 1);
-        issue_pv(1, j);
-        if (j + 1 < nb) issue_s(1, j + 1);
+        ring += 2 * nb;
+        gb += nb;
       }
     }
   } else {
     // ------------------------------------------------------------ softmax
-    constexpr int KEYS = BLK_N / SPLIT;       // key columns per softmax thread
-    const int x = warp / (4 * SPLIT);         // tile
-    const int hh = SPLIT == 1 ? 0 : (warp >> 2) & 1;  // key-column half
-    const int col0 = hh * KEYS;
+    const int x = warp / 4;                   // tile
     const int m = (warp & 3) * 32 + lane;     // TMEM lane / tile row
-    const int xbar = 1 + x * 4 + (warp & 3);  // named barrier of the row's two halves
     const int qi = m / p.G, hj = m % p.G;
-    const int a = (qb0 + x) * p.QB + qi;
-    const bool valid = a < p.A;
-    const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : maxpos;
     const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-    float m_used = -INFINITY, l = 0.f;
-    uint32_t r[KEYS];
-    for (int j = 0; j < nb; ++j) {
-      mbar_wait(bar_sfull(x), (uint32_t)(j & 1));
-      __syncwarp();
-      tc_fence_after();
-      if constexpr (SCHED == 4) {  // timing probe (wrong values): MMA + TMA pipeline alone
-        l = 1.f;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(bar_pfull(x));
-        continue;
-      }
-#pragma unroll
-      for (int c = 0; c < KEYS / 32; ++c) tmem_ld32(tS(x) + lane_off + col0 + c * 32, r + c * 32);
-#pragma unroll
-      for (int c = 0; c < KEYS / 32; ++c) tmem_wait_ld32(r + c * 32);
-      const int kbase = j * BLK_N + col0;
-      const bool need_mask = kbase + KEYS - 1 > pos;
-      if (need_mask) {
-#pragma unroll
-        for (int c = 0; c < KEYS; ++c)
-          if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
-      }
-      float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < KEYS; c += 8) {
-#pragma unroll
-        for (int t = 0; t < 4; ++t)
-          mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
-      }
-      float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
-      if constexpr (SPLIT == 2) {
-        // both halves of the row must use the same running max: exchange the
-        // block maxima (double buffered by block parity, so a fast half never
-        // overwrites a value its partner has not read yet)
-        float* xb = xch + (((j & 1) * 2 + x) * 2) * 128;
-        xb[hh * 128 + m] = mx;
-        named_bar_sync(xbar, 64);
-        mx = fmaxf(mx, xb[(hh ^ 1) * 128 + m]);  // symmetric: both halves get the same value
-      }
-      const float m_new = fmaxf(m_used, mx);
-      const bool grow = m_new > m_used + p.lazy_thresh;
-      const bool any_grow = __any_sync(0xffffffffu, grow);
-      const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
-      if (grow) m_used = m_new;
-      const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
-      const uint64_t nm2 = pk2(-m_used, -m_used);
-      uint64_t acc2[2] = {pk2(0.f, 0.f), pk2(0.f, 0.f)};
-      // P_j (bf16x2) -> TMEM columns [0, 64) of S_x, 32 keys per store
-      if constexpr (SCHED == 0 && SPLIT == 1) {
-        auto chunk = [&](auto cc) {
-          constexpr int c = decltype(cc)::value;
-          uint32_t pk[16];
-          if (need_mask)
-            softmax_chunks<32, 0u>(r + c * 32, sc2, nm2, acc2, pk);
-          else
-            softmax_chunks<32, (POLY_MASK >> (4 * c)) & 0xFu>(r + c * 32, sc2, nm2, acc2, pk);
-          tmem_st16(tS(x) + lane_off + c * 16, pk);
-        };
-        chunk(std::integral_constant<int, 0>{});
-        chunk(std::integral_constant<int, 1>{});
-        chunk(std::integral_constant<int, 2>{});
-        chunk(std::integral_constant<int, 3>{});
-      } else {
-        // phased, per half block (64 keys): the FFMA2 arguments, then the exp2
-        // run back to back (MUFU / polynomial), then packing + row sums + TMEM
-        // stores, so one warp keeps the MUFU pipe fed without per-chunk chains
-#pragma unroll
-        for (int hb = 0; hb < KEYS / 64; ++hb) {
-          uint32_t* rh = r + hb * 64;
-#pragma unroll
-          for (int c = 0; c < 64; c += 2) {
-            const uint64_t a2 = ffma2(pk2(__uint_as_float(rh[c]), __uint_as_float(rh[c + 1])), sc2, nm2);
-            float a, b;
-            upk2(a2, a, b);
-            rh[c] = __float_as_uint(a);
-            rh[c + 1] = __float_as_uint(b);
-          }
-          if (SCHED == 3) {  // timing probe (wrong values): exp2 replaced by an FMUL
-#pragma unroll
-            for (int c = 0; c < 64; ++c) rh[c] = __float_as_uint(__uint_as_float(rh[c]) * 0.5f);
-          } else if (need_mask) {
-#pragma unroll
-            for (int c = 0; c < 64; ++c) rh[c] = __float_as_uint(ex2(__uint_as_float(rh[c])));
-          } else {
-#pragma unroll
-            for (int c = 0; c < 64; c += 2) {
-              if ((POLY_MASK >> ((col0 + hb * 64 + c) / 8)) & 1) {
-                uint32_t o0, o1;
-                exp2_poly2(pk2(__uint_as_float(rh[c]), __uint_as_float(rh[c + 1])), o0, o1);
-                rh[c] = o0;
-                rh[c + 1] = o1;
-              } else {
-                rh[c] = __float_as_uint(ex2(__uint_as_float(rh[c])));
-                rh[c + 1] = __float_as_uint(ex2(__uint_as_float(rh[c + 1])));
-              }
-            }
-          }
-#pragma unroll
-          for (int c = 0; c < 2; ++c) {
-            uint32_t pk[16];
-#pragma unroll
-            for (int t = 0; t < 16; ++t) {
-              const uint32_t e0 = rh[c * 32 + 2 * t], e1 = rh[c * 32 + 2 * t + 1];
-              acc2[t & 1] = fadd2(acc2[t & 1], (uint64_t)e0 | ((uint64_t)e1 << 32));
-              pk[t] = pack_bf16(__uint_as_float(e0), __uint_as_float(e1));
-            }
-            tmem_st16(tS(x) + lane_off + col0 + (hb * 2 + c) * 16, pk);
-          }
-        }
-      }
-      {
-        float s0, s1, s2, s3;
-        upk2(acc2[0], s0, s1);
-        upk2(acc2[1], s2, s3);
-        l = l * corr + ((s0 + s1) + (s2 + s3));
-      }
-      tmem_wait_st();
-      if (any_grow && j > 0) {
-        // O_x *= corr once PV_x(j-1) has landed (warp-uniform branch)
-        mbar_wait(bar_pvdone(x), (uint32_t)((j - 1) & 1));
+    const uint64_t sc2 = pk2(p.scale_log2, p.scale_log2);
+    int gb = 0;
+    for (int i = 0;; ++i) {
+      const int u = unit_index(i, cta, grid);
+      if (u >= n_units) break;
+      const Unit w = unit_of(p, u);
+      const int a = (w.qb0 + x) * p.QB + qi;
+      const bool valid = a < p.A;
+      const int pos = valid ? min(__ldg(p.qpos + a), p.n_ctx - 1) : w.maxpos;
+      float m_used = -INFINITY, l = 0.f;
+      uint32_t r[BLK_N];
+      for (int j = 0; j < w.nb; ++j) {
+        const uint32_t par = (uint32_t)((gb + j) & 1);
+        mbar_wait(bar_sfull(x), par);
         __syncwarp();
         tc_fence_after();
-#pragma unroll 1
-        for (int c = 0; c < HD / 32 / SPLIT; ++c) {
-          const uint32_t oc = hh * (HD / SPLIT) + c * 32;
-          uint32_t o[32];
-          tmem_ld32(tO(x) + lane_off + oc, o);
-          tmem_wait_ld32(o);
+        CT_TRACE(0, x, j, i == 0 && (warp & 3) == 0 && lane == 0);
+        const int kbase = j * BLK_N;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-          tmem_st32(tO(x) + lane_off + oc, o);
+        for (int c = 0; c < 4; ++c) tmem_ld32(tS(x) + lane_off + 32 * c, r + 32 * c);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_wait_ld32(r + 32 * c);
+        // the diagonal block(s) of a row: keys past its position -> -inf.
+        // Warp-uniform branch (no divergence); such blocks stay all-MUFU so
+        // masked keys give exactly 0.
+        const bool masked = __any_sync(0xffffffffu, kbase + BLK_N - 1 > pos);
+        if (masked) {
+#pragma unroll
+          for (int c = 0; c < BLK_N; ++c)
+            if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
         }
-        tmem_wait_st();
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar_pfull(x));
-    }
-    mbar_wait(bar_pvdone(x), (uint32_t)((nb - 1) & 1));
-    __syncwarp();
-    tc_fence_after();
-    if constexpr (SPLIT == 2) {
-      float* xb = xch + (((nb & 1) * 2 + x) * 2) * 128;
-      xb[hh * 128 + m] = l;
-      named_bar_sync(xbar, 64);
-      l = l + xb[(hh ^ 1) * 128 + m];  // commutative: both halves agree
-    }
-    const float inv = valid ? 1.f / l : 0.f;
-    const int64_t orow = ((int64_t)a * p.Hq + (int64_t)g * p.G + hj) * HD;
+        float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < BLK_N; c += 8) {
+#pragma unroll
+          for (int t = 0; t < 4; ++t)
+            mq[t] = max3f(mq[t], __uint_as_float(r[c + 2 * t]), __uint_as_float(r[c + 2 * t + 1]));
+        }
+        const float mx = max3f(mq[0], mq[1], fmaxf(mq[2], mq[3])) * p.scale_log2;
+        const float m_new = fmaxf(m_used, mx);
+        const bool grow = m_new > m_used + p.lazy_thresh;
+        const bool any_grow = __any_sync(0xffffffffu, grow);
+        const float corr = grow ? ex2(m_used - m_new) : 1.f;  // 0 when m_used = -inf
+        if (grow) m_used = m_new;
+        const uint64_t nm2 = pk2(-m_used, -m_used);
+        // P = 2^(s*scale - m): the four 32-key chunks advance in lockstep so
+        // the MUFU exp2 of three chunks and the FMA-pipe polynomial exp2 of
+        // the POLY chunk (unmasked blocks) issue interleaved from one warp,
+        // with the argument FFMA2s, bf16 packing and FADD2 row sums in the
+        // gaps of the 8-cycle MUFU issue.
+        if (any_grow && j > 0) {
+          // O_x *= corr once PV_x(j-1) has landed (warp-uniform branch)
+          mbar_wait(bar_pvdone(x), (uint32_t)((gb + j - 1) & 1));
+          __syncwarp();
+          tc_fence_after();
 #pragma unroll 1
-    for (int cc = 0; cc < HD / 32 / SPLIT; ++cc) {
-      const int c = hh * (HD / 32 / SPLIT) + cc;
-      uint32_t o[32];
-      tmem_ld32(tO(x) + lane_off + c * 32, o);
-      tmem_wait_ld32(o);
-      if (valid) {
-        if (p.out_f32) {
-          float4* dst = reinterpret_cast<float4*>(p.out_f32 + orow + c * 32);
+          for (int c = 0; c < HD / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(tO(x) + lane_off + c * 32, o);
+            tmem_wait_ld32(o);
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
-                                 __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
-        } else {
-          uint4* dst = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+            tmem_st32(tO(x) + lane_off + c * 32, o);
+          }
+          tmem_wait_st();
+        }
+        // P in two key halves: the MMA warp starts PV on keys [0, 64) while
+        // this warp exponentiates keys [64, 128)
+        float bsum = 0.f;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            uint4 v;
-            v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
-            v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
-            v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
-            v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
-            dst[e] = v;
+        for (int h = 0; h < 2; ++h) {
+          uint32_t pk[32];
+          if (masked || POLY_MASK == 0)
+            bsum += p_half<0u>(r + 64 * h, sc2, nm2, pk);
+          else if (h == 0)
+            bsum += p_half<POLY_MASK & 3u>(r, sc2, nm2, pk);
+          else
+            bsum += p_half<(POLY_MASK >> 2) & 3u>(r + 64, sc2, nm2, pk);
+          tmem_st16(tS(x) + lane_off + 32 * h, pk);
+          tmem_st16(tS(x) + lane_off + 32 * h + 16, pk + 16);
+          tmem_wait_st();
+          tc_fence_before();
+          __syncwarp();
+          CT_TRACE(h == 1 ? 1 : 4, x, j, i == 0 && (warp & 3) == 0 && lane == 0);
+          CT_TRACE(8 + (warp & 3), x, j, h == 0 && i == 0 && lane == 0);
+          if (lane == 0) mbar_arrive(bar_pfull(x, h));
+          if (h == 0) {
+            // Re-read keys [64, 128) (their S columns are never overwritten by
+            // P): the true dependency keeps the second half's exp2 behind the
+            // first half's hand-off, which the scheduler would otherwise sink
+            // below all the MUFU work.
+            tmem_ld32(tS(x) + lane_off + 64, r + 64);
+            tmem_ld32(tS(x) + lane_off + 96, r + 96);
+            tmem_wait_ld32(r + 64);
+            tmem_wait_ld32(r + 96);
+            if (masked) {
+#pragma unroll
+              for (int c = 64; c < BLK_N; ++c)
+                if (kbase + c > pos) r[c] = __float_as_uint(-INFINITY);
+            }
+          }
+        }
+        l = l * corr + bsum;
+      }
+      // epilogue: O_x / l -> global once PV_x(nb-1) has landed
+      mbar_wait(bar_pvdone(x), (uint32_t)((gb + w.nb - 1) & 1));
+      __syncwarp();
+      tc_fence_after();
+      const float inv = valid ? 1.f / l : 0.f;
+      const int64_t orow = ((int64_t)a * p.Hq + (int64_t)w.g * p.G + hj) * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD / 32; ++c) {
+        uint32_t o[32];
+        tmem_ld32(tO(x) + lane_off + c * 32, o);
+        tmem_wait_ld32(o);
+        if (valid) {
+          if (p.out_f32) {
+            float4* dst = reinterpret_cast<float4*>(p.out_f32 + orow + c * 32);
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              dst[e] = make_float4(__uint_as_float(o[4 * e]) * inv, __uint_as_float(o[4 * e + 1]) * inv,
+                                   __uint_as_float(o[4 * e + 2]) * inv, __uint_as_float(o[4 * e + 3]) * inv);
+          } else {
+            uint4* dst = reinterpret_cast<uint4*>(p.out + orow + c * 32);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              uint4 v;
+              v.x = pack_bf16(__uint_as_float(o[8 * e + 0]) * inv, __uint_as_float(o[8 * e + 1]) * inv);
+              v.y = pack_bf16(__uint_as_float(o[8 * e + 2]) * inv, __uint_as_float(o[8 * e + 3]) * inv);
+              v.z = pack_bf16(__uint_as_float(o[8 * e + 4]) * inv, __uint_as_float(o[8 * e + 5]) * inv);
+              v.w = pack_bf16(__uint_as_float(o[8 * e + 6]) * inv, __uint_as_float(o[8 * e + 7]) * inv);
+              dst[e] = v;
+            }
           }
         }
       }
+      // the O reads above precede this warp's first pfull arrive of the next
+      // unit, which the PV that overwrites O_x (accumulate = 0) waits for
+      gb += w.nb;
     }
   }
   tc_fence_before();
@@ -1203,9 +682,48 @@ static int make_map(CUtensorMap* map, const void* ptr, uint64_t d1, uint64_t d2,
   return CT_OK;
 }
 
+// Process-wide knobs, read once.  CT_TC_LAZY: rescale threshold (log2 units,
+// default 8); CT_TC_POLY=<0,1,2,4,5,8>: which of
+// the four 32-key chunks of a block take the FMA-pipe exp2 (all values are
+// correct; 0 = all MUFU).
+struct TcKnobs {
+  float lazy = LAZY_THRESH;
+  int poly = 0;
+  TcKnobs() {
+    if (const char* e = getenv("CT_TC_LAZY")) lazy = (float)atof(e);
+    if (const char* e = getenv("CT_TC_POLY")) poly = (int)strtol(e, nullptr, 0) & 15;
+  }
+};
+static const TcKnobs& knobs() {
+  static const TcKnobs k;
+  return k;
+}
+
+static int sm_count() {
+  static int n = [] {
+    int dev = 0, v = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return 148;
+    }
+    return v;
+  }();
+  return n;
+}
+
 }  // namespace tc
 
-bool tc_enabled() { return true; }
+// tcgen05 preconditions: D = 128, GQA group divides the 128-row tile, 16-byte
+// aligned operands and rows (TMA).  Otherwise the SIMT kernel runs.
+bool tc_supported(const void* q, const void* k_cache, const void* v_cache, int64_t Hq,
+                  int64_t Hkv, int64_t D, int64_t cache_row_stride) {
+  if (D != tc::HD || Hkv < 1 || Hq % Hkv) return false;
+  const int64_t G = Hq / Hkv;
+  if (G < 1 || tc::TILE_M % G) return false;
+  if (((uintptr_t)q | (uintptr_t)k_cache | (uintptr_t)v_cache) & 15) return false;
+  return (cache_row_stride * 2) % 16 == 0;
+}
 
 size_t attention_tc_workspace(int64_t, int64_t, int64_t, int64_t, int64_t) { return 0; }
 
@@ -1216,24 +734,21 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   using namespace tc;
   (void)workspace;
   (void)workspace_bytes;
-  if (D != HD) return fail(CT_ERR_UNSUPPORTED, "tcgen05 attention needs head_dim 128");
+  if (!tc_supported(q, k_cache, v_cache, Hq, Hkv, D, cache_row_stride))
+    return fail(CT_ERR_UNSUPPORTED, "tcgen05 attention preconditions not met");
   const int64_t G = Hq / Hkv;
-  if (G < 1 || TILE_M % G) return fail(CT_ERR_UNSUPPORTED, "GQA group %lld must divide 128", (long long)G);
-  if (((uintptr_t)q | (uintptr_t)k_cache | (uintptr_t)v_cache) & 15)
-    return fail(CT_ERR_PARAM, "tensors must be 16-byte aligned");
-  if ((cache_row_stride * 2) % 16) return fail(CT_ERR_PARAM, "cache row stride alignment");
   CUtensorMap mq, mk, mv;
   int rc;
   if ((rc = make_map(&mq, q, (uint64_t)Hq, (uint64_t)A, HD * 2, (uint64_t)Hq * HD * 2,
                      (uint32_t)G, (uint32_t)(TILE_M / G))))
     return rc;
-  const int kbox = (getenv("CT_TC_CTAS") && atoi(getenv("CT_TC_CTAS")) == 2) ? BLK_N / 2 : BLK_N;
   if ((rc = make_map(&mk, k_cache, (uint64_t)Hkv, (uint64_t)n_ctx, HD * 2,
-                     (uint64_t)cache_row_stride * 2, 1, (uint32_t)kbox)))
+                     (uint64_t)cache_row_stride * 2, 1, BLK_N)))
     return rc;
   if ((rc = make_map(&mv, v_cache, (uint64_t)Hkv, (uint64_t)n_ctx, HD * 2,
                      (uint64_t)cache_row_stride * 2, 1, BLK_N)))
     return rc;
+  const TcKnobs& kn = knobs();
   Params prm;
   prm.qpos = q_pos;
   prm.out = out_dtype == CT_BF16 ? (__nv_bfloat16*)out : nullptr;
@@ -1246,82 +761,40 @@ int attention_tc(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq, con
   prm.n_ctx = (int)n_ctx;
   prm.n_qblocks = (int)((A + prm.QB - 1) / prm.QB);
   prm.scale_log2 = (float)(scale * 1.4426950408889634);
-  prm.lazy_thresh = LAZY_THRESH;
-  if (const char* e = getenv("CT_TC_LAZY")) prm.lazy_thresh = (float)atof(e);
-  // Single-CTA tiles by default.  CT_TC_CTAS=2 selects the CTA-pair kernel
-  // (cta_group::2, MMA M = 256, half of every K/V tile per SM): correct and it
-  // halves L2->SM traffic, but measured 40 % slower (its 2-SM TMA pipeline
-  // starves the MMA; profiles/round1_attention_variants.md).  CT_TC_EXPT /
-  // CT_TC_POLY are profiling aids.
-  int ctas = 1;
-  if (const char* e = getenv("CT_TC_CTAS")) ctas = atoi(e) == 2 ? 2 : 1;
-  // exp2 on MUFU only: with the phased softmax the FMA-pipe polynomial no
-  // longer pays (profiles/round1_attention_variants.md); CT_TC_POLY selects it
-  uint32_t poly = 0;
-  if (const char* e = getenv("CT_TC_POLY")) poly = (uint32_t)strtoul(e, nullptr, 0);
-  int expt = 0;
-  if (const char* e = getenv("CT_TC_EXPT")) expt = atoi(e);
+  prm.lazy_thresh = kn.lazy;
   using KernFn = void (*)(CUtensorMap, CUtensorMap, CUtensorMap, Params);
-  KernFn kern;
-  int pp = 1;
-  if (const char* e = getenv("CT_TC_PP")) pp = atoi(e);
-  if (pp && ctas == 1 && expt == 0) {
-    int sched = 1;
-    if (const char* e = getenv("CT_TC_SCHED")) sched = atoi(e);
-    KernFn kp = sched == 0 ? (poly == 0x4444 ? attention_pp_kernel<0x4444u, 0> : attention_pp_kernel<0u, 0>)
-              : sched == 3 ? attention_pp_kernel<0u, 3>
-              : sched == 4 ? attention_pp_kernel<0u, 4>
-              : poly == 0x3333 ? attention_pp_kernel<0x3333u>
-              : poly == 0x7777 ? attention_pp_kernel<0x7777u>
-              : poly == 0xFFFF ? attention_pp_kernel<0xFFFFu>
-              : poly == 0x4444 ? attention_pp_kernel<0x4444u>
-              : poly == 0x0202 ? attention_pp_kernel<0x0202u>
-              : poly == 0x5555 ? attention_pp_kernel<0x5555u>
-              : poly == 0x1111 ? attention_pp_kernel<0x1111u>
-              : poly == 0x2222 ? attention_pp_kernel<0x2222u> : attention_pp_kernel<0u>;
-    int split = 1;
-    if (const char* e = getenv("CT_TC_SPLIT")) split = atoi(e) == 2 ? 2 : 1;
-    // split rows (neutral on the selective shape; the FMA-pipe polynomial in
-    // the key half of one warp set measured much slower,
-    // profiles/round1_attention_variants.md)
-    if (split == 2) kp = attention_pp_kernel<0u, 1, 2, 4>;
-    const size_t smem_pp = (split == 2 ? SmemPP<4>::TOTAL : SmemPP<5>::TOTAL) + 1024;
-    CT_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_pp));
-    const unsigned grid_pp = (unsigned)(((prm.n_qblocks + 1) / 2) * Hkv);
-    kp<<<grid_pp, 32 * (8 * split + 2), smem_pp, st>>>(mq, mk, mv, prm);
-    return check_launch("attention_pp_kernel");
+  KernFn kp;
+  switch (kn.poly) {
+    case 0: kp = attention_pp_kernel<0u>; break;
+    case 1: kp = attention_pp_kernel<1u>; break;
+    case 2: kp = attention_pp_kernel<2u>; break;
+    case 4: kp = attention_pp_kernel<4u>; break;
+    case 8: kp = attention_pp_kernel<8u>; break;
+    case 5: kp = attention_pp_kernel<5u>; break;
+    default: return fail(CT_ERR_PARAM, "CT_TC_POLY=%d is not built (0, 1, 2, 4, 5, 8)", kn.poly);
   }
-  if (ctas == 2)
-    kern = expt == 1 ? attention_tc_kernel<2, 0, 1, 2> : expt == 2 ? attention_tc_kernel<2, 0, 2, 2>
-         : expt == 3 ? attention_tc_kernel<2, 0, 3, 2> : expt == 4 ? attention_tc_kernel<2, 0, 4, 2>
-         : poly == 0x22 ? attention_tc_kernel<2, 0x22, 0, 2> : attention_tc_kernel<2, 0, 0, 2>;
-  else
-    kern = expt == 1 ? attention_tc_kernel<2, 0, 1, 1> : expt == 2 ? attention_tc_kernel<2, 0, 2, 1>
-         : expt == 4 ? attention_tc_kernel<2, 0, 4, 1>
-         : poly == 0x22 ? attention_tc_kernel<2, 0x22, 0, 1> : attention_tc_kernel<2, 0, 0, 1>;
-  const size_t smem = (ctas == 2 ? Smem<2>::TOTAL : Smem<1>::TOTAL) + 1024;
-  const int threads = 32 * (4 * 2 + 2);
-  CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const int units = (prm.n_qblocks + ctas - 1) / ctas;
-  const unsigned grid = (unsigned)(units * Hkv * ctas);
-  if (ctas == 1) {
-    kern<<<grid, threads, smem, st>>>(mq, mk, mv, prm);
-  } else {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    CT_CUDA(cudaLaunchKernelEx(&cfg, kern, mq, mk, mv, prm));
+  const size_t smem = SmemPP::TOTAL + 1024;
+  CT_CUDA(cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int n_units = ((prm.n_qblocks + 1) / 2) * prm.Hkv;
+  const unsigned grid = (unsigned)std::min(n_units, sm_count());
+  kp<<<grid, 32 * 10, smem, st>>>(mq, mk, mv, prm);
+#ifdef CT_ATT_TRACE
+  if (const char* path = getenv("CT_TC_TRACE_OUT")) {
+    static unsigned long long h[14][2][512];
+    cudaStreamSynchronize(st);
+    cudaMemcpyFromSymbol(h, g_trace, sizeof(h));
+    if (FILE* f = fopen(path, "w")) {
+      for (int j = 0; j < 512; ++j)
+        for (int x = 0; x < 2; ++x) {
+          fprintf(f, "%d %d ", j, x);
+          for (int e = 0; e < 14; ++e) fprintf(f, "%s%llu", e ? " " : "", h[e][x][j]);
+          fprintf(f, "\n");
+        }
+      fclose(f);
+    }
   }
-  return check_launch("attention_tc_kernel");
+#endif
+  return check_launch("attention_pp_kernel");
 }
 
 }  // namespace ct

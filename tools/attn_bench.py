@@ -25,9 +25,13 @@ def main():
     ap.add_argument("--qscale", type=float, default=1.0)
     ap.add_argument("--full", action="store_true")
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--lib", default="", help="alternative libcachetune_b200.so (A/B)")
+    ap.add_argument("--dump", default="", help="save the output tensor (bit-identity A/B)")
     ap.add_argument("--rows", type=int, default=0,
                     help="only the last ROWS query rows (the few-row split-key path)")
     args = ap.parse_args()
+    if args.lib:
+        _lib._lib = _lib.load(args.lib)
     hq, hkv, d = 32, 8, 128
     rng = np.random.default_rng(0)
     if args.full:
@@ -66,6 +70,8 @@ def main():
     torch.cuda.synchronize()
     ms = s.elapsed_time(e) / args.iters
     kv_gbs = 2 * n * hkv * d * 2 / ms / 1e6
+    if args.dump:
+        torch.save(out.cpu(), args.dump)
     print(f"attention {'full' if args.full else 'selective'} A={a} n_ctx={n} qscale={args.qscale}: "
           f"{ms:.3f} ms  {flops / ms / 1e9:.1f} TFLOP/s  (K+V once: {kv_gbs:.0f} GB/s)")
 
