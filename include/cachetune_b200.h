@@ -108,6 +108,31 @@ int ct_score_chunk(const void* keys, const void* values, int dtype,
                    int32_t* agg_order, void* workspace, size_t workspace_bytes,
                    void* stream);
 
+/* Fast scorer with a certified selection boundary (N = 2048, lanes a
+ * multiple of 128; other geometries return CT_ERR_UNSUPPORTED and the caller
+ * uses ct_score_chunks).  The aggregate scores of ct/spectral.py:149-159 are
+ * computed with single-precision FFTs (relative error bound `guard`, see
+ * DESIGN.md); agg_order [C][N] is their stable descending order with the
+ * boundary between positions k-1 and k made exact: when the k-th and
+ * (k+1)-th scores are within the guard, every token whose score could cross
+ * the boundary is re-scored in float64 (direct projection, all layers) and
+ * that window re-ordered, so agg_order[0..k) is the float64 top-k set
+ * (ct/spectral.py:162-178).  wcount [C] (device int32): 0 = boundary
+ * certified by the guard, w in (0, 64] = w tokens re-scored exactly,
+ * w > 64 = window too wide, the caller must re-score the chunk with
+ * ct_score_chunks (exact mode).  layer_scores [C][L][N] f64 (nullable) and
+ * agg_scores [C][N] f64 are the single-precision-derived scores (window
+ * tokens carry their float64 aggregate).  Asynchronous, no host sync.
+ * band 0 = low band (default), 1 = high band. */
+size_t ct_score_fast_workspace_bytes(int64_t C, int64_t L, int64_t N, int64_t lanes);
+int ct_score_select_fast(const void* keys, const void* values, int dtype,
+                         int64_t C, int64_t L, int64_t N, int64_t lanes,
+                         int64_t ld_token, int64_t ld_layer, int64_t ld_chunk,
+                         int64_t cutoff, int band, int64_t k, double guard,
+                         double* layer_scores, double* agg_scores,
+                         int32_t* agg_order, int32_t* wcount, void* workspace,
+                         size_t workspace_bytes, void* stream);
+
 /* Stable descending argsort of `rows` rows of n f64 scores (ties -> lower
  * index): ct/spectral.py:99-101.  order is int32 [rows][n]. */
 int ct_desc_order(const double* scores, int64_t rows, int64_t n,

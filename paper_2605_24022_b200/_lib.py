@@ -64,6 +64,11 @@ _SIGS = {
                                      c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_size_t,
                                      c_void_p]),
     "ct_desc_order": (c_int, [c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "ct_score_fast_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64]),
+    "ct_score_select_fast": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64,
+                                     c_int64, c_int64, c_int64, c_int64, c_int64, c_int,
+                                     c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
+                                     c_void_p, c_size_t, c_void_p]),
     "ct_score_chunk": (c_int, [c_void_p, c_void_p, c_int, c_int64, c_int64, c_int64, c_int64,
                                c_int64, c_double, c_void_p, c_void_p, c_void_p, c_void_p,
                                c_size_t, c_void_p]),

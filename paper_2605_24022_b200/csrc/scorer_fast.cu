@@ -1,0 +1,628 @@
+// Fast scorer: single-precision four-step FFT energy kernel + certified top-k
+// boundary.  Same quantity as ct/spectral.py:69-79 / :149-159 (rfft along the
+// token axis, keep bins min(k, N-k) < c, irfft, per-token row norms, 0.5 K +
+// 0.5 V, sequential layer mean), computed for N = 2048 with float32 FFTs, and
+// a selection step that proves the top-k set of the aggregate score equals
+// the float64 one (ct/spectral.py:162-184):
+//
+//   1. fs_energy_kernel: two lanes packed per complex signal (the mask is
+//      Hermitian, so lowpass(a + ib) = lowpass(a) + i lowpass(b)); the 2048
+//      tokens are n = n2 + 64 n1.  Step 1: 32-point DFT over n1 in registers
+//      (radix-4/2 DIF, compile-time twiddles) and the W_2048^(n2 k1) twiddle;
+//      exchange 1 through shared memory; step 2: per k1 a 64-point DFT over
+//      n2, the band mask, the 64-point inverse (the same stages reversed, no
+//      reordering), the inverse twiddle; exchange 2; step 3: 32-point inverse
+//      over k1 -> tokens n2' + 64 n1', |y|^2 accumulated per token in
+//      registers over the CTA's signals.  Two shared-memory exchanges per
+//      signal (XOR-swizzled, at most 2 lanes per 8-byte bank slot), K/V read
+//      once with sector-complete 32-byte row pieces.
+//   2. fs_combine: per token and layer 0.5 sqrt(EK) + 0.5 sqrt(EV) in f64,
+//      sequential layer sum / L.
+//   3. desc order (scorer.cu), then fs_window: the aggregate scores carry a
+//      relative error bound g (calibrated); the k-th / (k+1)-th
+//      boundary is certified when a_k (1 - g) > a_{k+1} (1 + g); otherwise
+//      every token whose score lies in [a_{k+1}(1-g)/(1+g), a_k(1+g)/(1-g)]
+//      is re-scored exactly (fs_rescore: float64 direct low-pass projection
+//      y_i = sum_n p[(i - n) mod N] x_n over all layers, lanes and both
+//      tensors) and the window is re-ordered by (exact score desc, index asc)
+//      (fs_fixup).  Tokens outside the window provably keep their side of the
+//      boundary, so order[0..k) is the exact top-k set.  Windows wider than
+//      FS_WMAX tokens are reported; the host re-scores those chunks with the
+//      exact (float64) scorer.
+#include "common.cuh"
+
+namespace ct {
+namespace fs {
+
+constexpr int N = 2048;
+constexpr int THREADS = 256;
+constexpr int SIG_PER_BATCH = 8;
+constexpr int BATCHES = 8;                       // signals per CTA = 64 (128 lanes)
+constexpr int SIG_PER_CTA = SIG_PER_BATCH * BATCHES;
+constexpr int WMAX = 64;                         // window tokens re-scored per chunk
+
+__device__ constexpr float kCos64[64] = {
+#include "scorer_fast_cos64.inc"
+};
+__device__ constexpr float kSin64[64] = {
+#include "scorer_fast_sin64.inc"
+};
+
+// complex f32 as float2: adds / subs / twiddle products are packed FADD2 /
+// FMUL2 / FFMA2 (one issue slot per complex add, two per complex product)
+using cf = float2;
+__device__ __forceinline__ cf operator+(cf a, cf b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ cf operator-(cf a, cf b) {
+  return __fadd2_rn(a, make_float2(-b.x, -b.y));
+}
+// a * (i * SG), SG = +-1
+template <int SG>
+__device__ __forceinline__ cf mul_i(cf a) {
+  return SG > 0 ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
+}
+// a * exp(SG * 2 pi i * m / 64) with exact trivial factors
+template <int SG, int M>
+__device__ __forceinline__ cf tw64(cf a) {
+  constexpr int m = ((M % 64) + 64) % 64;
+  if constexpr (m == 0) {
+    return a;
+  } else if constexpr (m == 16) {
+    return mul_i<SG>(a);
+  } else if constexpr (m == 32) {
+    return make_float2(-a.x, -a.y);
+  } else if constexpr (m == 48) {
+    return mul_i<-SG>(a);
+  } else {
+    // (x c - y s, x s + y c) = x (c, s) + y (-s, c)
+    const float c = kCos64[m], s = SG * kSin64[m];
+    const cf r = __fmul2_rn(make_float2(a.x, a.x), make_float2(c, s));
+    return __ffma2_rn(make_float2(a.y, a.y), make_float2(-s, c), r);
+  }
+}
+__device__ __forceinline__ cf cmul(cf a, cf w) {
+  const cf r = __fmul2_rn(make_float2(a.x, a.x), w);
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(-w.y, w.x), r);
+}
+__device__ __forceinline__ cf cmulc(cf a, cf w) {  // a * conj(w)
+  const cf r = __fmul2_rn(make_float2(a.x, a.x), make_float2(w.x, -w.y));
+  return __ffma2_rn(make_float2(a.y, a.y), make_float2(w.y, w.x), r);
+}
+
+// Radix-4 DIF stage of span SPAN over v[M] (SG = -1: forward DFT kernel).
+template <int M, int SPAN, int SG>
+__device__ __forceinline__ void dif_stage(cf (&v)[M]) {
+  constexpr int Q = SPAN / 4, F = 64 / SPAN;
+#pragma unroll
+  for (int g = 0; g < M; g += SPAN) {
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const cf a = v[g + j], b = v[g + j + Q], c = v[g + j + 2 * Q], d = v[g + j + 3 * Q];
+      const cf t0 = a + c, t1 = a - c, t2 = b + d, t3 = mul_i<SG>(b - d);
+      v[g + j] = t0 + t2;
+      v[g + j + Q] = t1 + t3;
+      v[g + j + 2 * Q] = t0 - t2;
+      v[g + j + 3 * Q] = t1 - t3;
+    }
+  }
+}
+// twiddles of a DIF stage (applied after its butterflies): position j + rQ
+// of each group times W_SPAN^(r j)
+template <int M, int SPAN, int SG, int J = 0>
+__device__ __forceinline__ void dif_twiddle(cf (&v)[M]) {
+  constexpr int Q = SPAN / 4, F = 64 / SPAN;
+  if constexpr (J < Q) {
+#pragma unroll
+    for (int g = 0; g < M; g += SPAN) {
+      v[g + J + Q] = tw64<SG, F * J>(v[g + J + Q]);
+      v[g + J + 2 * Q] = tw64<SG, F * 2 * J>(v[g + J + 2 * Q]);
+      v[g + J + 3 * Q] = tw64<SG, F * 3 * J>(v[g + J + 3 * Q]);
+    }
+    dif_twiddle<M, SPAN, SG, J + 1>(v);
+  }
+}
+// inverse of dif_stage + dif_twiddle (conjugate twiddles first, then the
+// transposed butterfly); unnormalised
+template <int M, int SPAN, int SG, int J = 0>
+__device__ __forceinline__ void dit_twiddle(cf (&v)[M]) {
+  constexpr int Q = SPAN / 4, F = 64 / SPAN;
+  if constexpr (J < Q) {
+#pragma unroll
+    for (int g = 0; g < M; g += SPAN) {
+      v[g + J + Q] = tw64<SG, F * J>(v[g + J + Q]);
+      v[g + J + 2 * Q] = tw64<SG, F * 2 * J>(v[g + J + 2 * Q]);
+      v[g + J + 3 * Q] = tw64<SG, F * 3 * J>(v[g + J + 3 * Q]);
+    }
+    dit_twiddle<M, SPAN, SG, J + 1>(v);
+  }
+}
+template <int M, int SPAN, int SG>
+__device__ __forceinline__ void dit_stage(cf (&v)[M]) {
+  constexpr int Q = SPAN / 4;
+#pragma unroll
+  for (int g = 0; g < M; g += SPAN) {
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const cf y0 = v[g + j], y1 = v[g + j + Q], y2 = v[g + j + 2 * Q], y3 = v[g + j + 3 * Q];
+      const cf t0 = y0 + y2, t2 = y0 - y2, t1 = y1 + y3, t3 = mul_i<SG>(y1 - y3);
+      v[g + j] = t0 + t1;
+      v[g + j + 2 * Q] = t0 - t1;
+      v[g + j + Q] = t2 + t3;
+      v[g + j + 3 * Q] = t2 - t3;
+    }
+  }
+}
+template <int M>
+__device__ __forceinline__ void radix2(cf (&v)[M]) {
+#pragma unroll
+  for (int g = 0; g < M; g += 2) {
+    const cf a = v[g], b = v[g + 1];
+    v[g] = a + b;
+    v[g + 1] = a - b;
+  }
+}
+
+// Forward DFT (natural order in, digit-reversed out) and its exact reverse
+// (digit-reversed in, natural out, conjugate kernel): M = 32 (4, 4, 2), 64 (4, 4, 4).
+template <int M>
+__device__ __forceinline__ void fwd(cf (&v)[M]) {
+  dif_stage<M, M, -1>(v);
+  dif_twiddle<M, M, -1>(v);
+  dif_stage<M, M / 4, -1>(v);
+  dif_twiddle<M, M / 4, -1>(v);
+  if constexpr (M == 64) {
+    dif_stage<M, 4, -1>(v);
+  } else {
+    radix2<M>(v);
+  }
+}
+template <int M>
+__device__ __forceinline__ void inv(cf (&v)[M]) {
+  if constexpr (M == 64) {
+    dit_stage<M, 4, 1>(v);
+  } else {
+    radix2<M>(v);
+  }
+  dit_twiddle<M, M / 4, 1>(v);
+  dit_stage<M, M / 4, 1>(v);
+  dit_twiddle<M, M, 1>(v);
+  dit_stage<M, M, 1>(v);
+}
+// frequency held at output position p of fwd<M> (digit reversal)
+template <int M>
+__host__ __device__ constexpr int digrev(int p) {
+  if (M == 64) return ((p & 3) << 4) | (p & 12) | (p >> 4);
+  // 32: digits (base 4, base 4, base 2) of the DIF order
+  return ((p & 1) << 4) | (((p >> 1) & 3) << 2) | (p >> 3);
+}
+
+// exchange buffer index (8-byte units): [s][k1][n2 ^ swz(s, k1)].  An 8-byte
+// access is served per half-warp (16 lanes x 8 B = one wavefront); in every
+// exchange pattern a half-warp holds 8 signal slots s and two k1 or two n2
+// values, and swz = 2s ^ (k1 & 1) maps them onto 16 distinct 8-byte slots.
+__device__ __forceinline__ int xidx(int s, int k1, int n2) {
+  return ((s * 32 + k1) << 6) + (n2 ^ ((s << 1) ^ (k1 & 1)));
+}
+
+template <typename IN>
+__device__ __forceinline__ cf load_pair(const IN* p);
+template <>
+__device__ __forceinline__ cf load_pair<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(p));
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+template <>
+__device__ __forceinline__ cf load_pair<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float2*>(p));
+}
+
+// grid: x = lane group (SIG_PER_CTA signals), y = tensor (0 K, 1 V), z = c*L + l.
+// partial[((c*L + l)*2 + tensor)*G + group][N] f32 (unnormalised |y|^2, x N^2)
+template <typename IN>
+__global__ void __launch_bounds__(THREADS, 1)
+fs_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int L,
+                 int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff, int high,
+                 const float2* __restrict__ tw, int groups, float* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cf* xb = reinterpret_cast<cf*>(smem_raw);                  // [8][32][64]
+  cf* T = xb + SIG_PER_BATCH * 32 * 64;                       // W_2048^m, m < 2048
+  const int t = threadIdx.x, s = t & 7, q = t >> 3;
+  const int tensor = blockIdx.y, group = blockIdx.x;
+  const int c = blockIdx.z / L, l = blockIdx.z % L;
+  for (int i = t; i < N; i += THREADS) T[i] = tw[i];
+  const IN* base = (tensor ? values : keys) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer +
+                   (int64_t)group * SIG_PER_CTA * 2;
+  // energies of tokens q + 32 (s >> 2) + 64 (8 (s & 3) + i), i < 8: the
+  // batch's |y|^2 of the 8 signal slots are reduce-scattered over the 8 lanes
+  // of one q, so each lane keeps 8 token sums instead of 64
+  float acc[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  __syncthreads();
+
+#pragma unroll 1
+  for (int b = 0; b < BATCHES; ++b) {
+    const IN* sig = base + (b * SIG_PER_BATCH + s) * 2;
+    // ---- step 1: 32-point DFT over n1 of tokens n2 + 64 n1, twiddle, exchange
+#pragma unroll
+    for (int jb = 0; jb < 2; ++jb) {
+      const int n2 = q + 32 * jb;
+      cf v[32];
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) v[n1] = load_pair<IN>(sig + (int64_t)(n2 + 64 * n1) * ld_token);
+      fwd<32>(v);
+#pragma unroll
+      for (int p = 0; p < 32; ++p) {
+        const int k1 = digrev<32>(p);
+        xb[xidx(s, k1, n2)] = cmul(v[p], T[(n2 * k1) & (N - 1)]);
+      }
+    }
+    __syncthreads();
+    // ---- step 2: per k1 = q: 64-point DFT over n2, band mask, inverse, twiddle
+    {
+      const int k1 = q;
+      cf u[64];
+#pragma unroll
+      for (int n2 = 0; n2 < 64; ++n2) u[n2] = xb[xidx(s, k1, n2)];
+      fwd<64>(u);
+#pragma unroll
+      for (int p = 0; p < 64; ++p) {
+        const int k = k1 + 32 * digrev<64>(p);
+        const int kk = min(k, N - k);
+        const bool keep = high ? kk >= cutoff : kk < cutoff;
+        if (!keep) u[p] = make_float2(0.f, 0.f);
+      }
+      inv<64>(u);
+      // this thread's row of the buffer is read and written by it alone
+#pragma unroll
+      for (int n2 = 0; n2 < 64; ++n2) xb[xidx(s, k1, n2)] = cmulc(u[n2], T[(n2 * k1) & (N - 1)]);
+    }
+    __syncthreads();
+    // ---- step 3: 32-point inverse over k1 -> tokens n2' + 64 n1', energies
+    float e[64];
+#pragma unroll
+    for (int jb = 0; jb < 2; ++jb) {
+      const int n2 = q + 32 * jb;
+      cf w[32];
+#pragma unroll
+      for (int p = 0; p < 32; ++p) w[p] = xb[xidx(s, digrev<32>(p), n2)];
+      inv<32>(w);
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) e[32 * jb + n1] = fmaf(w[n1].x, w[n1].x, w[n1].y * w[n1].y);
+    }
+    __syncthreads();
+    // reduce-scatter over s (xor 4, 2, 1): lane s ends with slots [8s, 8s + 8)
+    {
+      const bool b2 = s & 4, b1 = s & 2, b0 = s & 1;
+      float f[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float send = b2 ? e[i] : e[32 + i];
+        f[i] = (b2 ? e[32 + i] : e[i]) + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      float g2[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const float send = b1 ? f[i] : f[16 + i];
+        g2[i] = (b1 ? f[16 + i] : f[i]) + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float send = b0 ? g2[i] : g2[8 + i];
+        acc[i] += (b0 ? g2[8 + i] : g2[i]) + __shfl_xor_sync(0xffffffffu, send, 1);
+      }
+    }
+  }
+  float* out = partial + ((((int64_t)c * L + l) * 2 + tensor) * groups + group) * N;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) out[q + 32 * (s >> 2) + 64 * (8 * (s & 3) + i)] = acc[i];
+}
+
+__global__ void fs_twiddle(float2* tw) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= N) return;
+  double sn, cs;
+  sincospi(2.0 * (double)m / (double)N, &sn, &cs);
+  tw[m] = make_float2((float)cs, (float)-sn);  // W_N^m = exp(-2 pi i m / N)
+}
+
+// layer score = 0.5 sqrt(EK) / N + 0.5 sqrt(EV) / N (f64, groups summed in
+// order), aggregate = sequential layer sum / L (ct/spectral.py:74-78,156)
+__global__ void fs_combine(const float* __restrict__ partial, int C, int L, int groups,
+                           double* __restrict__ layer_scores, double* __restrict__ agg) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= (int64_t)C * N) return;
+  const int c = (int)(i / N), n = (int)(i % N);
+  double acc = 0.0;
+  for (int l = 0; l < L; ++l) {
+    double e[2];
+    for (int t = 0; t < 2; ++t) {
+      const float* p = partial + (((int64_t)c * L + l) * 2 + t) * groups * N + n;
+      double s = 0.0;
+      for (int g = 0; g < groups; ++g) s += (double)p[(int64_t)g * N];
+      e[t] = s;
+    }
+    const double sc = 0.5 * (sqrt(e[0]) / (double)N) + 0.5 * (sqrt(e[1]) / (double)N);
+    if (layer_scores) layer_scores[((int64_t)c * L + l) * N + n] = sc;
+    acc += sc;
+  }
+  agg[i] = acc / (double)L;
+}
+
+// Per chunk: certify the boundary between order positions k-1 and k, or mark
+// the window of positions whose scores could cross it.  win[c] = {p0, p1}
+// (p1 < p0: certified / no boundary); wcount[c] = window size (0 certified,
+// > WMAX: too wide, the host re-scores the chunk exactly).
+__global__ void fs_window(const double* __restrict__ agg, const int32_t* __restrict__ order,
+                          int C, int k, double g, int2* __restrict__ win,
+                          int32_t* __restrict__ wcount) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double* a = agg + (int64_t)c * N;
+  const int32_t* o = order + (int64_t)c * N;
+  int2 w = make_int2(1, 0);
+  int cnt = 0;
+  if (k > 0 && k < N) {
+    const double ak = a[o[k - 1]], ak1 = a[o[k]];
+    if (!(ak * (1.0 - g) > ak1 * (1.0 + g))) {
+      const double vhi = ak * (1.0 + g) / (1.0 - g), vlo = ak1 * (1.0 - g) / (1.0 + g);
+      int p0 = k - 1, p1 = k;
+      while (p0 > 0 && a[o[p0 - 1]] <= vhi) --p0;
+      while (p1 < N - 1 && a[o[p1 + 1]] >= vlo) ++p1;
+      w = make_int2(p0, p1);
+      cnt = p1 - p0 + 1;
+    }
+  }
+  win[c] = w;
+  wcount[c] = cnt;
+}
+
+// p[m] = (1/N) sum_{k in band} w_k cos(2 pi k m / N): row of P = F^-1 M F
+__global__ void fs_kernel_row(int cutoff, int high, double* p) {
+  const int m = blockIdx.x * blockDim.x + threadIdx.x;
+  if (m >= N) return;
+  const int klo = high ? cutoff : 0, khi = high ? N / 2 : min(cutoff - 1, N / 2);
+  double s = 0.0;
+  for (int k = klo; k <= khi; ++k) {
+    const int km = (int)(((long long)k * m) % N);
+    s += ((k == 0 || 2 * k == N) ? 1.0 : 2.0) * cospi(2.0 * (double)km / (double)N);
+  }
+  p[m] = s / (double)N;
+}
+
+// Exact (float64) energy of the window tokens of one (chunk, layer, tensor):
+// y_w[lane] = sum_n p[(i_w - n) mod N] x[n][lane], E_w = sum_lanes y_w^2.
+// grid: x = chunk (chunks without a re-score window exit), y = tensor,
+// z = layer; 128 threads x 8 lanes (one 16-byte bf16 row piece per tap), R
+// window tokens per pass: one pass over the rows serves R tokens, and the
+// warp-uniform p values are shared-memory broadcasts.
+constexpr int RS_THREADS = 512, RS_LPT = 2, RS_UNROLL = 8;
+template <typename IN>
+__device__ __forceinline__ float2 load2(const IN* p);
+template <>
+__device__ __forceinline__ float2 load2<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(p));
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+template <>
+__device__ __forceinline__ float2 load2<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float2*>(p));
+}
+template <int R, typename IN>
+__device__ __forceinline__ void rescore_pass(const IN* __restrict__ x, int lanes, int64_t ld_token,
+                                             const double* ps, const int* tok, int nr,
+                                             double (*red)[8], double* out) {
+  double part[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) part[r] = 0.0;
+  for (int lane0 = threadIdx.x * RS_LPT; lane0 < lanes; lane0 += RS_THREADS * RS_LPT) {
+    double y[R][RS_LPT];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < RS_LPT; ++i) y[r][i] = 0.0;
+    for (int n0 = 0; n0 < N; n0 += RS_UNROLL) {
+      float2 xv[RS_UNROLL];  // RS_UNROLL rows in flight
+#pragma unroll
+      for (int u = 0; u < RS_UNROLL; ++u) xv[u] = load2<IN>(x + (int64_t)(n0 + u) * ld_token + lane0);
+#pragma unroll
+      for (int u = 0; u < RS_UNROLL; ++u) {
+        const double x4[RS_LPT] = {(double)xv[u].x, (double)xv[u].y};
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const double pv = ps[(tok[r] - n0 - u) & (N - 1)];
+#pragma unroll
+          for (int i = 0; i < RS_LPT; ++i) y[r][i] = fma(pv, x4[i], y[r][i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int i = 0; i < RS_LPT; ++i) part[r] = fma(y[r][i], y[r][i], part[r]);
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    double v = part[r];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5][r] = v;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < nr) {
+    double v = 0.0;
+    for (int wi = 0; wi < RS_THREADS / 32; ++wi) v += red[wi][threadIdx.x];
+    out[threadIdx.x] = v;
+  }
+  __syncthreads();
+}
+template <typename IN>
+__global__ void __launch_bounds__(RS_THREADS)
+fs_rescore(const IN* __restrict__ keys, const IN* __restrict__ values, int L, int lanes,
+           int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, const double* __restrict__ p,
+           const int2* __restrict__ win, const int32_t* __restrict__ wcount,
+           const int32_t* __restrict__ order, double* __restrict__ wenergy) {
+  const int c = blockIdx.x;
+  const int W = wcount[c];
+  if (W <= 0 || W > WMAX) return;
+  __shared__ double ps[N];
+  __shared__ double red[RS_THREADS / 32][8];  // [warp][token]
+  __shared__ double res[8];
+  const int tensor = blockIdx.y, l = blockIdx.z;
+  const int2 w = win[c];
+  for (int i = threadIdx.x; i < N; i += RS_THREADS) ps[i] = p[i];
+  __syncthreads();
+  const IN* x = (tensor ? values : keys) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer;
+  for (int r0 = 0; r0 < W; r0 += 8) {
+    const int nr = min(8, W - r0);
+    int tok[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) tok[r] = r < nr ? order[(int64_t)c * N + w.x + r0 + r] : 0;
+    if (nr <= 2)
+      rescore_pass<2, IN>(x, lanes, ld_token, ps, tok, nr, red, res);
+    else if (nr <= 4)
+      rescore_pass<4, IN>(x, lanes, ld_token, ps, tok, nr, red, res);
+    else
+      rescore_pass<8, IN>(x, lanes, ld_token, ps, tok, nr, red, res);
+    if ((int)threadIdx.x < nr)
+      wenergy[(((int64_t)c * WMAX + r0 + threadIdx.x) * L + l) * 2 + tensor] = res[threadIdx.x];
+  }
+}
+
+// Exact window scores -> window re-ordered by (score desc, index asc).
+__global__ void fs_fixup(int C, const int2* __restrict__ win, const int32_t* __restrict__ wcount,
+                         const double* __restrict__ wenergy, int L, int32_t* __restrict__ order,
+                         double* __restrict__ agg) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C || wcount[c] <= 0 || wcount[c] > WMAX) return;
+  const int slot = c;
+  const int2 w = win[c];
+  const int W = w.y - w.x + 1;
+  int32_t* o = order + (int64_t)c * N + w.x;
+  double sc[WMAX];
+  int id[WMAX];
+  for (int r = 0; r < W; ++r) {
+    double acc = 0.0;
+    for (int l = 0; l < L; ++l) {
+      const double* e = wenergy + (((int64_t)slot * WMAX + r) * L + l) * 2;
+      acc += 0.5 * sqrt(e[0]) + 0.5 * sqrt(e[1]);
+    }
+    sc[r] = acc / (double)L;
+    id[r] = o[r];
+  }
+  for (int i = 1; i < W; ++i) {  // insertion sort: desc score, asc index
+    const double s = sc[i];
+    const int t = id[i];
+    int j = i - 1;
+    while (j >= 0 && (sc[j] < s || (sc[j] == s && id[j] > t))) {
+      sc[j + 1] = sc[j];
+      id[j + 1] = id[j];
+      --j;
+    }
+    sc[j + 1] = s;
+    id[j + 1] = t;
+  }
+  for (int r = 0; r < W; ++r) {
+    o[r] = id[r];
+    agg[(int64_t)c * N + id[r]] = sc[r];
+  }
+}
+
+}  // namespace fs
+}  // namespace ct
+
+using namespace ct;
+
+extern "C" int ct_desc_order(const double* scores, int64_t rows, int64_t n, int32_t* order,
+                             void* stream);
+
+static size_t fs_groups(int64_t lanes) { return (size_t)(lanes / (2 * fs::SIG_PER_CTA)); }
+
+extern "C" size_t ct_score_fast_workspace_bytes(int64_t C, int64_t L, int64_t N, int64_t lanes) {
+  if (N != fs::N || lanes % (2 * fs::SIG_PER_CTA)) return 0;
+  size_t b = align_up((size_t)C * L * 2 * fs_groups(lanes) * N * sizeof(float), 256);
+  b += align_up((size_t)N * sizeof(float2), 256);                 // twiddles
+  b += align_up((size_t)N * sizeof(double), 256);                 // projection row
+  b += align_up((size_t)C * sizeof(int2), 256);                   // windows
+  b += align_up((size_t)C * fs::WMAX * L * 2 * sizeof(double), 256);  // window energies
+  return b;
+}
+
+extern "C" int ct_score_select_fast(const void* keys, const void* values, int dtype, int64_t C,
+                                    int64_t L, int64_t N, int64_t lanes, int64_t ld_token,
+                                    int64_t ld_layer, int64_t ld_chunk, int64_t cutoff, int band,
+                                    int64_t k, double guard, double* layer_scores,
+                                    double* agg_scores, int32_t* agg_order, int32_t* wcount,
+                                    void* workspace, size_t workspace_bytes, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  if (C < 1 || L < 1 || lanes < 1)
+    return fail(CT_ERR_SHAPE, "score geometry C=%lld L=%lld lanes=%lld", (long long)C,
+                (long long)L, (long long)lanes);
+  if (N != fs::N || lanes % (2 * fs::SIG_PER_CTA))
+    return fail(CT_ERR_UNSUPPORTED, "fast scorer needs N = %d and lanes %% %d == 0 (N=%lld)",
+                fs::N, 2 * fs::SIG_PER_CTA, (long long)N);
+  if (!valid_dtype(dtype)) return fail(CT_ERR_PARAM, "dtype %d", dtype);
+  if (band != 0 && band != 1) return fail(CT_ERR_PARAM, "band %d", band);
+  if (cutoff < 0 || cutoff > N / 2 + 1) return fail(CT_ERR_PARAM, "cutoff %lld", (long long)cutoff);
+  if (k < 0 || k > N) return fail(CT_ERR_PARAM, "k %lld", (long long)k);
+  if (!(guard >= 0.0 && guard < 0.5)) return fail(CT_ERR_PARAM, "guard %g", guard);
+  if (!keys || !values || !agg_scores || !agg_order || !wcount)
+    return fail(CT_ERR_PARAM, "null tensor");
+  if (C * L > 65535) return fail(CT_ERR_UNSUPPORTED, "C*L too large");
+  if (workspace_bytes < ct_score_fast_workspace_bytes(C, L, N, lanes))
+    return fail(CT_ERR_PARAM, "workspace too small");
+  const int groups = (int)fs_groups(lanes);
+  char* ws = (char*)workspace;
+  float* partial = (float*)ws;
+  ws += align_up((size_t)C * L * 2 * groups * N * sizeof(float), 256);
+  float2* tw = (float2*)ws;
+  ws += align_up((size_t)N * sizeof(float2), 256);
+  double* prow = (double*)ws;
+  ws += align_up((size_t)N * sizeof(double), 256);
+  int2* win = (int2*)ws;
+  ws += align_up((size_t)C * sizeof(int2), 256);
+  double* wenergy = (double*)ws;
+  int rc;
+  fs::fs_twiddle<<<(fs::N + 255) / 256, 256, 0, st>>>(tw);
+  if ((rc = check_launch("fs_twiddle"))) return rc;
+  const size_t smem = (size_t)fs::SIG_PER_BATCH * 32 * 64 * sizeof(fs::cf) + fs::N * sizeof(fs::cf);
+  dim3 grid((unsigned)groups, 2, (unsigned)(C * L));
+  if (dtype == CT_BF16) {
+    auto kern = fs::fs_energy_kernel<__nv_bfloat16>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, fs::THREADS, smem, st>>>((const __nv_bfloat16*)keys, (const __nv_bfloat16*)values,
+                                          (int)L, ld_token, ld_layer, ld_chunk, (int)cutoff, band,
+                                          tw, groups, partial);
+  } else {
+    auto kern = fs::fs_energy_kernel<float>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, fs::THREADS, smem, st>>>((const float*)keys, (const float*)values, (int)L,
+                                          ld_token, ld_layer, ld_chunk, (int)cutoff, band, tw,
+                                          groups, partial);
+  }
+  if ((rc = check_launch("fs_energy_kernel"))) return rc;
+  fs::fs_combine<<<(unsigned)((C * fs::N + 255) / 256), 256, 0, st>>>(partial, (int)C, (int)L,
+                                                                      groups, layer_scores,
+                                                                      agg_scores);
+  if ((rc = check_launch("fs_combine"))) return rc;
+  if ((rc = ct_desc_order(agg_scores, C, N, agg_order, stream))) return rc;
+  fs::fs_window<<<(unsigned)((C + 127) / 128), 128, 0, st>>>(agg_scores, agg_order, (int)C,
+                                                             (int)k, guard, win, wcount);
+  if ((rc = check_launch("fs_window"))) return rc;
+  // every chunk gets re-score CTAs; the ones without a window (or with one
+  // wider than FS_WMAX, which the caller re-scores exactly) exit at once, so
+  // the call never waits for the window counts on the host
+  fs::fs_kernel_row<<<(fs::N + 255) / 256, 256, 0, st>>>((int)cutoff, band, prow);
+  if ((rc = check_launch("fs_kernel_row"))) return rc;
+  dim3 rgrid((unsigned)C, 2, (unsigned)L);
+  if (dtype == CT_BF16)
+    fs::fs_rescore<__nv_bfloat16><<<rgrid, fs::RS_THREADS, 0, st>>>(
+        (const __nv_bfloat16*)keys, (const __nv_bfloat16*)values, (int)L, (int)lanes, ld_token,
+        ld_layer, ld_chunk, prow, win, wcount, agg_order, wenergy);
+  else
+    fs::fs_rescore<float><<<rgrid, fs::RS_THREADS, 0, st>>>((const float*)keys, (const float*)values, (int)L,
+                                                 (int)lanes, ld_token, ld_layer, ld_chunk, prow,
+                                                 win, wcount, agg_order, wenergy);
+  if ((rc = check_launch("fs_rescore"))) return rc;
+  fs::fs_fixup<<<(unsigned)((C + 63) / 64), 64, 0, st>>>((int)C, win, wcount, wenergy, (int)L,
+                                                         agg_order, agg_scores);
+  return check_launch("fs_fixup");
+}

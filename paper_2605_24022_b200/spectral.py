@@ -150,6 +150,72 @@ def score_device(keys: torch.Tensor, values: torch.Tensor, alpha: float = DEFAUL
     return out
 
 
+# Relative error bound of the single-precision aggregate scores of
+# ct_score_select_fast (calibrated on model-encoded and Gaussian chunks,
+# DESIGN.md "Fast scorer"), and the widest boundary window re-scored on the
+# device (wider windows fall back to the exact scorer for that chunk).
+FAST_GUARD = 2e-6
+FAST_WMAX = 64
+
+
+def score_select_fast(keys: torch.Tensor, values: torch.Tensor, k: int,
+                      alpha: float = DEFAULT_ALPHA, guard: float = FAST_GUARD,
+                      band: str = "low", want_layer_scores: bool = False):
+    """Scores + an aggregate order whose first k entries are exactly the
+    float64 top-k set (ct/spectral.py:149-178), from single-precision FFTs
+    (ct_score_select_fast).  keys/values [C, L, 2048, H, D] (or [L, ...]) on
+    the device; H*D a multiple of 128.  Chunks whose boundary window is wider
+    than FAST_WMAX are re-scored with the exact float64 scorer (their whole
+    order is then exact).  Returns device tensors agg [C,N] f64, agg_order
+    [C,N] int32, wcount [C] int32 (0 = certified by the guard, w = w tokens
+    re-scored, -1 = exact fallback) and layer_scores [C,L,N] (or None)."""
+    _check_alpha(alpha)
+    if band not in ("low", "high"):
+        raise InvalidParam(f"band must be 'low' or 'high', got {band!r}")
+    if keys.shape != values.shape:
+        raise ShapeError(f"keys {tuple(keys.shape)} vs values {tuple(values.shape)}")
+    if keys.dim() == 4:
+        keys, values = keys.unsqueeze(0), values.unsqueeze(0)
+    if keys.dim() != 5:
+        raise ShapeError("expected [C, L, N, H, D]")
+    keys, values = keys.contiguous(), values.contiguous()
+    C, L, N, H, D = keys.shape
+    if not 0 <= k <= N:
+        raise InvalidParam(f"k must be in [0, {N}], got {k}")
+    lanes = H * D
+    dev = keys.device
+    cutoff = cutoff_index(alpha, N // 2 + 1)
+    lib = _lib.load()
+    wsb = lib.ct_score_fast_workspace_bytes(C, L, N, lanes)
+    if wsb == 0:
+        raise _lib.Unsupported(f"fast scorer needs N = 2048 and H*D % 128 == 0 (N={N})")
+    out = {
+        "agg": torch.empty((C, N), dtype=torch.float64, device=dev),
+        "agg_order": torch.empty((C, N), dtype=torch.int32, device=dev),
+        "wcount": torch.empty(C, dtype=torch.int32, device=dev),
+        "layer_scores": (torch.empty((C, L, N), dtype=torch.float64, device=dev)
+                         if want_layer_scores else None),
+    }
+    ws = _dev.workspace(wsb, "score_fast")
+    _lib.check(lib.ct_score_select_fast(
+        _dev.ptr(keys), _dev.ptr(values), _dev.ct_dtype(keys.dtype), C, L, N, lanes, lanes,
+        N * lanes, L * N * lanes, cutoff, 1 if band == "high" else 0, k, guard,
+        _dev.ptr(out["layer_scores"]), _dev.ptr(out["agg"]), _dev.ptr(out["agg_order"]),
+        _dev.ptr(out["wcount"]), _dev.ptr(ws), wsb, _dev.stream_handle()),
+        "ct_score_select_fast")
+    wide = torch.nonzero(out["wcount"] > FAST_WMAX).flatten().tolist()
+    if wide:  # pathological windows (ties, near-constant chunks): exact scorer
+        sel = torch.as_tensor(wide, device=dev)
+        ex = score_device(keys.index_select(0, sel), values.index_select(0, sel), alpha, "f64",
+                          want_layer_order=False, band=band)
+        out["agg"][sel] = ex["agg"]
+        out["agg_order"][sel] = ex["agg_order"]
+        if out["layer_scores"] is not None:
+            out["layer_scores"][sel] = ex["layer_scores"]
+        out["wcount"][sel] = -1
+    return out
+
+
 def low_freq_scores(keys, values, alpha: float = DEFAULT_ALPHA,
                     precision: str = "f64") -> np.ndarray:
     """Per-token importance (ct/spectral.py:82-90): 0.5|K~_i| + 0.5|V~_i|."""
