@@ -220,6 +220,29 @@ def all_host_threads():
         return contextlib.nullcontext()
 
 
+def host_info() -> dict:
+    """CPU model, core counts, numpy / BLAS versions and the thread environment
+    the CPU arm ran with."""
+    info = {"cpu_count": os.cpu_count(), "affinity": cpu_threads(),
+            "threads_env": {k: os.environ.get(k) for k in
+                            ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}}
+    try:
+        for line in Path("/proc/cpuinfo").read_text().splitlines():
+            if line.startswith("model name"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    info["numpy"] = np.__version__
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{k: d.get(k) for k in ("internal_api", "version", "num_threads")}
+                        for d in threadpool_info() if d.get("user_api") == "blas"]
+    except ImportError:  # pragma: no cover
+        pass
+    return info
+
+
 def run_reference(args, rank, world):
     c = CONFIGS[args.config]
     if rank != 0:
@@ -240,7 +263,7 @@ def run_reference(args, rank, world):
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": c["desc"], "sample": desc},
         "cpu_baseline": {"value": val, "unit": "requests/s", "cores": cpu_threads(),
-                         "kind": "port", "sample": desc},
+                         "kind": "port", "sample": desc, "host": host_info()},
         "e2e": {"value": val, "unit": "requests/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
@@ -457,7 +480,7 @@ def run_ours(args, rank, world, local_rank):
         with all_host_threads():
             sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
         cpu = {"value": 1.0 / sec, "unit": "requests/s", "cores": cpu_threads(), "kind": "port",
-               "sample": desc}
+               "sample": desc, "host": host_info()}
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -657,7 +680,7 @@ def run_batch(args, rank, world, local_rank):
         with all_host_threads():
             sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
         cpu = {"value": 1.0 / sec, "unit": "requests/s", "cores": cpu_threads(), "kind": "port",
-               "sample": desc}
+               "sample": desc, "host": host_info()}
     line = {
         "metric": METRIC, "value": n_req * args.steps / (total * 1e-3), "unit": "requests/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -680,6 +703,39 @@ def run_batch(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def self_launch(n: int) -> int:
+    """Re-exec this script under torch.distributed.run with n ranks on this
+    node (rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # communicator sizes in the log (nranks check)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
+def run_dry(args, rank, world):
+    """The launch / reduction plumbing of run_ours without the workload."""
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    ms = torch.tensor([(time.perf_counter() - t0) * 1e3], dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": world,
+                          "ms_max_over_ranks": float(ms[0]), "steps": args.steps,
+                          "warmup": args.warmup}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -690,12 +746,25 @@ def main():
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=32)
+    ap.add_argument("--dry-run", action="store_true",
+                    help="plumbing only: rank/world handling and the max-over-ranks line, "
+                         "no GPU work (CPU test of the multi-rank launch)")
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        # `bench.py --gpus N` outside torchrun: launch the N ranks ourselves
+        # (one process per GPU) instead of silently measuring one GPU
+        sys.exit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} disagrees with WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, rank, max(world, args.gpus))
+        return
+    if args.dry_run:
+        run_dry(args, rank, world)
         return
     if world > 1:
         import torch

@@ -41,3 +41,33 @@ def test_reference_arm_other_ranks_silent():
     p = _run({"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
     assert p.returncode == 0, p.stderr[-2000:]
     assert not [l for l in p.stdout.splitlines() if l.startswith("{")]
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun launches two ranks itself (one per
+    GPU; gloo plumbing run here) and rank 0 reports n_gpus = 2 with the
+    max-over-ranks time -- the driver's scaling run cannot silently measure
+    one GPU."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run",
+                        "--steps", "1", "--warmup", "0"], cwd=ROOT, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [l for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["dry_run"] is True
+    assert d["ms_max_over_ranks"] >= 19.0  # rank 1 sleeps 20 ms: the max, not rank 0's
+
+
+def test_gpus_flag_disagreeing_with_world_size_fails():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--dry-run"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=120)
+    assert p.returncode == 2 and "disagrees" in p.stderr
+
+
+def test_reference_arm_reports_host_info():
+    d = json.loads([l for l in _run().stdout.splitlines() if l.startswith("{")][0])
+    host = d["cpu_baseline"]["host"]
+    assert host["cpu_count"] >= 1 and host["numpy"] and "threads_env" in host
