@@ -281,7 +281,7 @@ class CachePool:
             stored = self._stored(cid)
             host = self.get_full(cid)
             src = tokens[i] if tokens is not None else stored.source_tokens
-            src = np.zeros(host.token_count, np.int64) if src is None else np.asarray(src)
+            src = None if src is None else np.asarray(src)  # None: fetch-only chunk
             host = KvChunk(cid, host.keys_raw, host.values, host.dtype_code, src)
             chunks.append(DeviceChunk.from_host(host, dtype=dtype, device=dev))
             ranks.append(stored.ranking)

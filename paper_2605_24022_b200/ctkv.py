@@ -124,9 +124,9 @@ def pool_from_ctkv(files, location: str = "pinned", dtype=torch.bfloat16, tokens
         chunk, rk = read_ctkv(data, cid)
         if rk is None:
             raise InvalidPlan(f"{cid} has no ranking block; analyze it first")
+        # without source tokens the chunk stays fetch-only: engines refuse to
+        # recompute it (InvalidPlan) instead of recomputing token id 0
         src = None if tokens is None else np.asarray(tokens[i], dtype=np.int64)
-        if src is None:
-            src = np.zeros(chunk.token_count, np.int64)
         chunk = KvChunk(chunk.chunk_id, chunk.keys_raw, chunk.values, chunk.dtype_code, src)
         chunks.append(DeviceChunk.from_host(chunk, dtype=dtype, device=device))
         ranks.append(rk)

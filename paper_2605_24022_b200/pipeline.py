@@ -23,6 +23,7 @@ import numpy as np
 import torch
 
 from . import _dev, _lib
+from .errors import InvalidPlan
 from .model import GpuModel
 from .pool import KvPool
 from .prefill import NORM_EPS, LayerBuffers, run_layers  # noqa: F401
@@ -137,6 +138,10 @@ class SelectivePrefillEngine:
         idx = [pool.chunk_index(c) for c in chunk_ids]
         if len(idx) != C:
             raise ValueError(f"request needs exactly {C} chunks, got {len(idx)}")
+        for ci in idx:  # ct/toymodel.py:243-244
+            if self.k and not pool.has_tokens[ci]:
+                raise InvalidPlan(f"chunk {pool.chunk_ids[ci]!r} lacks source_tokens; "
+                                  "cannot recompute")
         if self.graph is not None and idx != self.chunk_ids:
             raise RuntimeError("bind() would change a captured graph's parameters")
         self.chunk_ids = idx
@@ -155,7 +160,8 @@ class SelectivePrefillEngine:
                 src = [pool.tail_ptr(ci, l, self.k) for ci in idx]
                 self.copy_args.append(((ctypes.c_void_p * C)(*dst), (ctypes.c_void_p * C)(*src),
                                        (ctypes.c_int64 * C)(*([nbytes] * C))))
-        # per-layer K3 segments (kernel parameters)
+        # per-layer K3 segments (kernel parameters), in launches of at most
+        # CT_MAX_SEGMENTS segments each
         self.segs = []
         for l in range(L):
             segs = []
@@ -165,7 +171,9 @@ class SelectivePrefillEngine:
                 base = self.stage[l, c].data_ptr() if self.pinned else pool.tail_ptr(ci, l, self.k)
                 tok = self.agg.data_ptr() + (c * N + self.k) * 4
                 segs.append(_lib.Segment(base, base + H * D * esz, tok, self.n_keep, c * N, 0))
-            self.segs.append((_lib.Segment * max(len(segs), 1))(*segs) if segs else None)
+            groups = [segs[i:i + _lib.CT_MAX_SEGMENTS]
+                      for i in range(0, len(segs), _lib.CT_MAX_SEGMENTS)]
+            self.segs.append([((_lib.Segment * len(g))(*g), len(g)) for g in groups])
 
     # real three-stream timeline (ct/pipesim.py Timeline schema) ------------------
     def _ev(self, stream: str, layer: int, edge: int) -> torch.cuda.Event:
@@ -237,10 +245,11 @@ class SelectivePrefillEngine:
                 self._ev("forward", l, 0).record()   # fusion starts once transfer l landed
         t = self.timer.start("blend")
         pool = self.pool
-        _lib.call("ct_gather_rope_blend", self.segs[l], self.n_segs, 2 * self.row_elems,
-                  pool.H, pool.D, _dev.ct_dtype(pool.dtype),
-                  self.model.config.rope_params.pairing_code, _dev.ptr(self.table),
-                  _dev.ptr(self.cache[l, 0]), _dev.ptr(self.cache[l, 1]), self.row_elems, st)
+        for arr, n in self.segs[l]:
+            _lib.call("ct_gather_rope_blend", arr, n, 2 * self.row_elems,
+                      pool.H, pool.D, _dev.ct_dtype(pool.dtype),
+                      self.model.config.rope_params.pairing_code, _dev.ptr(self.table),
+                      _dev.ptr(self.cache[l, 0]), _dev.ptr(self.cache[l, 1]), self.row_elems, st)
         self.timer.stop("blend", t)
 
     def step(self, suffix=None, logits_out: torch.Tensor | None = None,

@@ -72,11 +72,22 @@ class KvPool:
         self.esize = torch.empty((), dtype=self.dtype).element_size()
         self.row_bytes = H * D * self.esize
         self.agg = torch.stack([rk.aggregate_device(self.device) for rk in rankings]).contiguous()
-        self.tokens = torch.stack([
-            c.tokens if c.tokens is not None else
-            torch.as_tensor(np.asarray(c.source_tokens, np.int32), device=self.device)
-            for c in chunks]).contiguous()
-        self.tokens_host = np.stack([np.asarray(c.source_tokens, np.int64) for c in chunks])
+        # source token ids per chunk; a chunk restored from a CTKV file without
+        # them (the format does not carry tokens, ct/kvcore.py:121-123) serves
+        # sparse fetches but cannot be recomputed (engines raise InvalidPlan,
+        # ct/toymodel.py:243-244)
+        self.has_tokens = [c.tokens is not None or c.source_tokens is not None for c in chunks]
+
+        def dev_tokens(c):
+            if c.tokens is not None:
+                return c.tokens
+            if c.source_tokens is not None:
+                return torch.as_tensor(np.asarray(c.source_tokens, np.int32), device=self.device)
+            return torch.zeros(N, dtype=torch.int32, device=self.device)  # never read
+        self.tokens = torch.stack([dev_tokens(c) for c in chunks]).contiguous()
+        self.tokens_host = np.stack([np.asarray(c.source_tokens, np.int64)
+                                     if c.source_tokens is not None else np.zeros(N, np.int64)
+                                     for c in chunks])
         shape = (self.C, L, N, 2, H, D)
         dev_img = torch.empty(shape, dtype=self.dtype, device=self.device)
         tmp = torch.empty((N, H, D), dtype=self.dtype, device=self.device)
@@ -139,11 +150,14 @@ class KvPool:
     def measure_transfer_cost(self, tier, sample_bytes: int,
                               bytes_per_token: int | None = None) -> float:
         """t_i for `tier` exactly as the reference computes it (scheduler.calibrate
-        calls this when no profile is injected); bytes_per_token defaults to a
-        K+V row of this pool.  The B200 PCIe rate itself is measured by
-        scheduler.measure_h2d_per_token."""
+        calls this when no profile is injected); bytes_per_token defaults to
+        the reference's f32 K+V CTKV row.  The B200 PCIe rate itself is
+        measured by scheduler.measure_h2d_per_token."""
         if bytes_per_token is None:
-            bytes_per_token = self.row_bytes * 2
+            # the reference's CTKV row (f32 K + V, ct/cachepool.py:146-152,505),
+            # as cachepool.token_row_bytes and pipesim.layer_keep_bytes charge
+            # it -- not this pool's storage width
+            bytes_per_token = self.H * self.D * 4 * 2
         return transfer_cost_per_token(tier, sample_bytes, bytes_per_token)
 
     def fetch_sparse(self, plan: SparseFetchPlan, stream=None):
@@ -156,27 +170,32 @@ class KvPool:
         if n_keep == 0:
             return None, None, plan.keep_indices
         k = self.N - n_keep
-        stage = torch.empty((n_keep, 2, self.H, self.D), dtype=self.dtype, device=self.device)
         src = self.tail_ptr(c, plan.layer, k)
         nbytes = plan.byte_ranges[0][1]
-        dst = (ctypes_ptr_array([stage.data_ptr()]), ctypes_ptr_array([src]),
-               ctypes_i64_array([nbytes]))
-        if self.location == "pinned":
-            _lib.call("ct_copy_ranges_h2d", dst[0], dst[1], dst[2], 1, _dev.stream_handle(stream))
-        else:
-            stage.view(-1).view(torch.uint8).copy_(
-                self.data.view(-1)[self.offset_bytes(c, plan.layer, k) // self.esize:
-                                   self.offset_bytes(c, plan.layer, k) // self.esize
-                                   + nbytes // self.esize].view(torch.uint8))
+        # every allocation, copy and gather on ONE stream (the caller's, default
+        # current): the staging buffer's memory cannot be reused by another
+        # stream's allocation while the copy / gather still read it
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        with torch.cuda.stream(st):
+            stage = torch.empty((n_keep, 2, self.H, self.D), dtype=self.dtype, device=self.device)
+            if self.location == "pinned":
+                _lib.call("ct_copy_ranges_h2d", ctypes_ptr_array([stage.data_ptr()]),
+                          ctypes_ptr_array([src]), ctypes_i64_array([nbytes]), 1,
+                          _dev.stream_handle(st))
+            else:
+                off = self.offset_bytes(c, plan.layer, k) // self.esize
+                stage.view(-1).view(torch.uint8).copy_(
+                    self.data.view(-1)[off: off + nbytes // self.esize].view(torch.uint8))
+            # un-permute: output row i = token keep[i] = tail row rank[keep[i]] - k
+            rank = np.argsort(self.rankings[c].aggregate_order)
+            rows = torch.as_tensor((rank[plan.keep_indices] - k).astype(np.int32),
+                                   device=self.device)
+            kv = torch.empty_like(stage)
+            _lib.call("ct_gather_rows", _dev.ptr(stage), _dev.ptr(rows), n_keep,
+                      2 * self.row_bytes, _dev.ptr(kv), _dev.stream_handle(st))
         with self._stats_lock:
             self.io_stats["bytes_read"] += nbytes
             self.io_stats["reads"] += 1
-        # un-permute: output row i = token keep[i] = tail row rank[keep[i]] - k
-        rank = np.argsort(self.rankings[c].aggregate_order)
-        rows = torch.as_tensor((rank[plan.keep_indices] - k).astype(np.int32), device=self.device)
-        kv = torch.empty_like(stage)
-        _lib.call("ct_gather_rows", _dev.ptr(stage), _dev.ptr(rows), n_keep, 2 * self.row_bytes,
-                  _dev.ptr(kv), _dev.stream_handle(stream))
         return kv[:, 0], kv[:, 1], plan.keep_indices
 
 

@@ -27,7 +27,7 @@ from .errors import InvalidPlan, ShapeError
 from .kvcore import DeviceChunk, SeqTensor
 from .model import GpuModel
 from .rope import rope_table
-from .spectral import ImportanceRanking, select_device
+from .spectral import ImportanceRanking, select_device, selection_count
 
 NORM_EPS = 1e-6  # ct/toymodel.py:28
 
@@ -374,16 +374,27 @@ def selective_prefill(model, chunks: Sequence, rankings: Sequence, suffix_tokens
     g = as_gpu_model(model, dtype)
     cfg = g.config
     _validate(cfg, chunks, rankings)
+    # host-side selection (ct/toymodel.py:246-267) so the active token ids are
+    # validated before any device work (ct/toymodel.py:303), as the reference
+    # does, and the query positions need no device readback later
+    sizes = [c.token_count for c in chunks]
+    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    suffix = np.asarray(suffix_tokens, dtype=np.int64)
+    ks_host = [selection_count(r, n) for n in sizes]
+    rec_host = np.sort(np.concatenate(
+        [np.asarray(rk.aggregate_order[:k], np.int64) + off
+         for rk, k, off in zip(rankings, ks_host, offsets)] or [np.empty(0, np.int64)]))
+    src_host = np.concatenate([np.asarray(c.source_tokens, np.int64) for c in chunks])
+    qpos_host = np.concatenate([rec_host, np.arange(offsets[-1], offsets[-1] + suffix.size)])
+    if qpos_host.size:
+        _check_tokens(g, np.concatenate([src_host[rec_host], suffix]))
     dev = g.device
     dchunks = [c if isinstance(c, DeviceChunk) else DeviceChunk.from_host(c, g.dtype, dev)
                for c in chunks]
     for c in dchunks:
         if c.keys.dtype != g.dtype:
             raise ShapeError(f"chunk dtype {c.keys.dtype} != model dtype {g.dtype}")
-    sizes = [c.token_count for c in dchunks]
-    offsets = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
     history = int(offsets[-1])
-    suffix = np.asarray(suffix_tokens, dtype=np.int64)
     n_ctx = history + suffix.size
     aggs = [rk.aggregate_device(dev) if isinstance(rk, ImportanceRanking)
             else torch.as_tensor(np.asarray(rk.aggregate_order, np.int32), device=dev)
@@ -404,11 +415,6 @@ def selective_prefill(model, chunks: Sequence, rankings: Sequence, suffix_tokens
     if n_rec:
         _lib.call("ct_gather_rows", _dev.ptr(src_all), _dev.ptr(rec), n_rec, 4,
                   _dev.ptr(tokens), _dev.stream_handle())
-    qpos_host = positions.cpu().numpy().astype(np.int64)
-    if a:
-        # ct/toymodel.py:303 -- active token ids must be in the vocabulary
-        src_host = np.concatenate([np.asarray(c.source_tokens) for c in dchunks])
-        _check_tokens(g, np.concatenate([src_host[qpos_host[:n_rec]], suffix]))
     caches = _new_caches(g, n_ctx, dev)
     hkv, d = cfg.kv_heads, cfg.head_dim
     keep_base = np.concatenate([[0], np.cumsum([n - k for n, k in zip(sizes, ks)])])

@@ -198,3 +198,50 @@ def test_cachepool_fetch_sparse_bit_exact_into_hbm(ct, tmp_path, file_backed):
             if a[2].size:
                 assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
     assert len(geo) >= 1
+
+
+def test_engine_more_chunks_than_one_blend_launch(ct):
+    """80 chunks > CT_MAX_SEGMENTS (64): the engine splits each layer's blend
+    into launches of at most 64 segments and matches selective_prefill."""
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    from paper_2605_24022_b200.pool import KvPool
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=1024, seed=6)
+    m = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(6)
+    chunks = [ct.encode_chunk_isolated(m, rng.integers(0, 1024, size=64), chunk_id=f"s{j}")
+              for j in range(80)]
+    ranks = ct.rank_chunks(chunks)
+    suffix = torch.as_tensor(rng.integers(0, 1024, size=8).astype(np.int32), device="cuda")
+    eng = SelectivePrefillEngine(m, KvPool(chunks, ranks, "hbm"), 0.15, 8)
+    got = eng.step(suffix).float().cpu()
+    ref = ct.selective_prefill(m, chunks, ranks, suffix.cpu().numpy(), 0.15, logits_rows="last",
+                               record_attention=False)
+    assert torch.equal(ref.logits.float().cpu(), got)
+    assert torch.equal(ref.kv[0][0].float().cpu(), eng.cache[0, 0].float().cpu())
+
+
+def test_ctkv_pool_without_tokens_is_fetch_only(ct):
+    """A pool restored from CTKV files without source tokens serves fetches
+    but the engine refuses to recompute its chunks (ct/toymodel.py:243-244)
+    instead of recomputing token id 0."""
+    from paper_2605_24022_b200.ctkv import pool_from_ctkv, write_ctkv
+    from paper_2605_24022_b200.errors import InvalidPlan
+    from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=1024, seed=7)
+    m = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(7)
+    toks = [rng.integers(0, 1024, size=128) for _ in range(2)]
+    chunks = [ct.encode_chunk_isolated(m, t, chunk_id=f"f{j}") for j, t in enumerate(toks)]
+    ranks = ct.rank_chunks(chunks)
+    blobs = [write_ctkv(c.to_host(), rk) for c, rk in zip(chunks, ranks)]
+    pool = pool_from_ctkv(blobs, "hbm")
+    assert pool.has_tokens == [False, False]
+    plan = pool.plan_sparse_fetch(pool.chunk_ids[0], 1, 0.15)
+    K, V, keep = pool.fetch_sparse(plan)
+    assert K.shape[0] == plan.keep_count
+    with pytest.raises(InvalidPlan):
+        SelectivePrefillEngine(m, pool, 0.15, 8)
+    ok = pool_from_ctkv(blobs, "hbm", tokens=toks)
+    assert ok.has_tokens == [True, True]
+    SelectivePrefillEngine(m, ok, 0.15, 8).step(
+        torch.zeros(8, dtype=torch.int32, device="cuda"))
