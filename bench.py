@@ -243,6 +243,23 @@ def host_info() -> dict:
     return info
 
 
+def pinned_h2d_peak(dev) -> float:
+    """GB/s of one 1 GiB contiguous pinned-host -> HBM copy (best of 3)."""
+    import torch
+    src = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    dst = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    best = float("inf")
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        dst.copy_(src, non_blocking=True)
+        e.record()
+        e.synchronize()
+        best = min(best, s.elapsed_time(e))
+    del src, dst
+    return (1 << 30) / (best * 1e-3) / 1e9
+
+
 def run_reference(args, rank, world):
     c = CONFIGS[args.config]
     if rank != 0:
@@ -312,15 +329,18 @@ def run_ours(args, rank, world, local_rank):
     scorers = {"f64": lambda: score_device(keys, vals, 0.5, "f64", want_layer_order=False),
                "fast": lambda: score_select_fast(keys, vals, k_sel)}
     for prec, fn in scorers.items():
-        fn()  # warm-up
-        torch.cuda.synchronize()
-        es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        es.record()
-        for _ in range(2):
+        for _ in range(2):  # warm-up (first launches load the kernels)
+            fn()
+        ms_list = []
+        for _ in range(5):  # median of individually timed calls
+            torch.cuda.synchronize()
+            es, ee = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            es.record()
             out = fn()
-        ee.record()
-        torch.cuda.synchronize()
-        sc_times[prec] = es.elapsed_time(ee) / 2
+            ee.record()
+            torch.cuda.synchronize()
+            ms_list.append(es.elapsed_time(ee))
+        sc_times[prec] = statistics.median(ms_list)
         if prec == "f64":
             agg_rows = out["agg_order"]
         else:  # the certified top-k sets must be the exact ones
@@ -340,7 +360,8 @@ def run_ours(args, rank, world, local_rank):
     del keys, vals
 
     pool_hbm = KvPool(chunks, rankings, "hbm", device=dev)
-    pool_pin = KvPool(chunks, rankings, "pinned", device=dev)
+    pool_pin = KvPool(chunks, rankings, "pinned", device=dev,
+                      resident_layers=args.resident_layers)
     del chunks
     torch.cuda.empty_cache()
     timer = KernelTimer()
@@ -392,6 +413,11 @@ def run_ours(args, rank, world, local_rank):
     qkv_ms = timer.mean_ms("qkv")
     # ---- e2e: pinned host pool, H2D keep rows + tokens, D2H logits, all timed
     e2e_ms, e2e_total = timed(lambda: eng_e2e.step(suffix_host, logits_host), args.steps)
+    # sparse transfer alone (copy engines, after the timed regions): one
+    # request's streamed keep tails, and a plain contiguous pinned H2D copy as
+    # the measured peak
+    h2d_ms = statistics.median(eng_e2e.time_transfer() for _ in range(3))
+    h2d_peak = pinned_h2d_peak(dev)
     ref_logits = eng.step(suffix_dev).float()
     torch.cuda.synchronize()
     agree = float((logits_host.to(dev) - ref_logits).abs().max() /
@@ -399,6 +425,9 @@ def run_ours(args, rank, world, local_rank):
     # ---- full-recompute baseline, same kernels
     full_ms = None
     e2e_h2d = eng_e2e.h2d_bytes
+    eng_ring = eng_e2e.ring
+    stage_bytes = eng_e2e.stage.numel() * eng_e2e.stage.element_size()
+    copies_per_req = (cfg.n_layers - eng_e2e.res) * eng_e2e.C
     if not args.no_full:
         del eng_e2e
         torch.cuda.empty_cache()
@@ -432,6 +461,7 @@ def run_ours(args, rank, world, local_rank):
     p50 = allmax(statistics.median(step_ms))
     p50_e2e = allmax(statistics.median(e2e_ms))
     full_ms = allmax(full_ms)
+    h2d_ms = allmax(h2d_ms)
     att_ms = allmax(att_ms)
     blend_ms = allmax(blend_ms)
     qkv_ms = allmax(qkv_ms)
@@ -535,6 +565,18 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": ncu_traffic("fs_energy_kernel", args.config)},
         },
         "step_tflops": step_flops / (p50 * 1e-3) / 1e12,
+        "sparse_h2d": {
+            "bound": "pcie", "bytes_per_request": e2e_h2d, "copy_engine_ms": h2d_ms,
+            "achieved": e2e_h2d / (h2d_ms * 1e-3) / 1e9 if h2d_ms else None,
+            "peak": h2d_peak, "unit": "GB/s",
+            "frac": (e2e_h2d / (h2d_ms * 1e-3) / 1e9 / h2d_peak) if h2d_ms else None,
+            "peak_source": "measured here: one 1 GiB pinned->device cudaMemcpyAsync, best of 3",
+            "exposed_ms": p50_e2e - p50,
+            "ring_slots": eng_ring, "stage_bytes": stage_bytes,
+            "resident_layers": args.resident_layers,
+            "copies_per_request": copies_per_req,
+            "note": "one cudaMemcpyAsync per (chunk, streamed layer) on a copy stream; exposed "
+                    "= e2e p50 - HBM-pool p50 (the transfer time not hidden by compute)"},
         "e2e": {"value": e2e_val, "unit": "requests/s", "p50_ttft_ms": p50_e2e,
                 "h2d_bytes_per_step": e2e_h2d + 4 * c["suffix"],
                 "d2h_bytes_per_step": 4 * cfg.vocab_size, "logits_match_hbm_path": agree},
@@ -746,6 +788,8 @@ def main():
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-rows", type=int, default=32)
+    ap.add_argument("--resident-layers", type=int, default=0,
+                    help="e2e arm: first n layers of the pinned pool also kept in HBM")
     ap.add_argument("--dry-run", action="store_true",
                     help="plumbing only: rank/world handling and the max-over-ranks line, "
                          "no GPU work (CPU test of the multi-rank launch)")

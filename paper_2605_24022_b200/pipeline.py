@@ -74,7 +74,8 @@ class SelectivePrefillEngine:
     reuses every device buffer."""
 
     def __init__(self, model: GpuModel, pool: KvPool, r: float, suffix_len: int,
-                 timer: KernelTimer | None = None, n_chunks: int | None = None):
+                 timer: KernelTimer | None = None, n_chunks: int | None = None,
+                 ring_layers: int = 4):
         cfg = model.config
         if (pool.L, pool.H, pool.D) != (cfg.n_layers, cfg.kv_heads, cfg.head_dim):
             raise ValueError("pool geometry disagrees with model")
@@ -110,12 +111,20 @@ class SelectivePrefillEngine:
                                 else "f32", dev)
         self.pinned = pool.location == "pinned"
         self.row_elems = H * D
+        # pinned pool: layers >= res stream over PCIe through a ring of
+        # `ring` staging slots (a layer's copy may start once the blend of
+        # the layer that last used its slot has run); layers < res are the
+        # pool's HBM-resident tier
+        self.res = pool.resident_layers if self.pinned else 0
+        self.ring = max(1, min(int(ring_layers), L - self.res)) if self.pinned else 0
         if self.pinned:
-            self.stage = torch.empty((L, C, max(self.n_keep, 1), 2, H, D), dtype=dt, device=dev)
+            self.stage = torch.empty((self.ring, C, max(self.n_keep, 1), 2, H, D), dtype=dt,
+                                     device=dev)
             self.copy_stream = torch.cuda.Stream(device=dev)
             self.copy_done = [torch.cuda.Event() for _ in range(L)]
+            self.slot_free = [torch.cuda.Event() for _ in range(L)]
             self.step_start = torch.cuda.Event()
-            self.h2d_bytes = L * C * self.n_keep * 2 * pool.row_bytes
+            self.h2d_bytes = (L - self.res) * C * self.n_keep * 2 * pool.row_bytes
         else:
             self.h2d_bytes = 0
         self.n_segs = C if self.n_keep else 0
@@ -154,12 +163,12 @@ class SelectivePrefillEngine:
         L, H, D, esz = pool.L, pool.H, pool.D, pool.esize
         if self.pinned:
             nbytes = self.n_keep * 2 * pool.row_bytes
-            self.copy_args = []
-            for l in range(L):
-                dst = [self.stage[l, c].data_ptr() for c in range(C)]
+            self.copy_args = [None] * L
+            for l in range(self.res, L):
+                dst = [self.stage[self._slot(l), c].data_ptr() for c in range(C)]
                 src = [pool.tail_ptr(ci, l, self.k) for ci in idx]
-                self.copy_args.append(((ctypes.c_void_p * C)(*dst), (ctypes.c_void_p * C)(*src),
-                                       (ctypes.c_int64 * C)(*([nbytes] * C))))
+                self.copy_args[l] = ((ctypes.c_void_p * C)(*dst), (ctypes.c_void_p * C)(*src),
+                                     (ctypes.c_int64 * C)(*([nbytes] * C)))
         # per-layer K3 segments (kernel parameters), in launches of at most
         # CT_MAX_SEGMENTS segments each
         self.segs = []
@@ -168,7 +177,12 @@ class SelectivePrefillEngine:
             for c, ci in enumerate(idx):
                 if self.n_keep == 0:
                     continue
-                base = self.stage[l, c].data_ptr() if self.pinned else pool.tail_ptr(ci, l, self.k)
+                if not self.pinned:
+                    base = pool.tail_ptr(ci, l, self.k)
+                elif l < self.res:
+                    base = pool.resident_tail_ptr(ci, l, self.k)
+                else:
+                    base = self.stage[self._slot(l), c].data_ptr()
                 tok = self.agg.data_ptr() + (c * N + self.k) * 4
                 segs.append(_lib.Segment(base, base + H * D * esz, tok, self.n_keep, c * N, 0))
             groups = [segs[i:i + _lib.CT_MAX_SEGMENTS]
@@ -235,14 +249,49 @@ class SelectivePrefillEngine:
         # read keep rows (K and V) + write them into the cache
         return 2 * 2 * self.C * self.n_keep * self.pool.row_bytes
 
+    def _slot(self, l: int) -> int:
+        return (l - self.res) % self.ring
+
+    def _issue_copy(self, l: int, after=None) -> None:
+        """Queue layer l's keep-tail copies (one cudaMemcpyAsync per chunk) on
+        the copy stream, after event `after` (the blend that freed its slot)."""
+        with torch.cuda.stream(self.copy_stream):
+            if after is not None:
+                self.copy_stream.wait_event(after)
+            if self.record_timeline:
+                self._ev("transfer", l, 0).record(self.copy_stream)
+            d, s, b = self.copy_args[l]
+            _lib.call("ct_copy_ranges_h2d", d, s, b, self.C, _dev.stream_handle(self.copy_stream))
+            self.copy_done[l].record(self.copy_stream)
+            if self.record_timeline:
+                self._ev("transfer", l, 1).record(self.copy_stream)
+
+    def time_transfer(self) -> float:
+        """ms of copy-engine time for one request's streamed keep tails alone
+        (every streamed layer back to back on the copy stream, no compute);
+        h2d_bytes / this = the achieved sparse-transfer rate."""
+        if not self.pinned or self.n_segs == 0 or self.res >= self.pool.L:
+            return 0.0
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        self.copy_stream.wait_stream(torch.cuda.current_stream())
+        s.record(self.copy_stream)
+        for l in range(self.res, self.pool.L):
+            d, src, b = self.copy_args[l]
+            _lib.call("ct_copy_ranges_h2d", d, src, b, self.C,
+                      _dev.stream_handle(self.copy_stream))
+        e.record(self.copy_stream)
+        e.synchronize()
+        return s.elapsed_time(e)
+
     def _reuse(self, l: int) -> None:
         if self.n_segs == 0:
             return
         st = _dev.stream_handle()
-        if self.pinned:
+        streamed = self.pinned and l >= self.res
+        if streamed:
             torch.cuda.current_stream().wait_event(self.copy_done[l])
-            if self.record_timeline:
-                self._ev("forward", l, 0).record()   # fusion starts once transfer l landed
+        if self.pinned and self.record_timeline:
+            self._ev("forward", l, 0).record()   # fusion starts once transfer l landed
         t = self.timer.start("blend")
         pool = self.pool
         for arr, n in self.segs[l]:
@@ -251,6 +300,10 @@ class SelectivePrefillEngine:
                       self.model.config.rope_params.pairing_code, _dev.ptr(self.table),
                       _dev.ptr(self.cache[l, 0]), _dev.ptr(self.cache[l, 1]), self.row_elems, st)
         self.timer.stop("blend", t)
+        if streamed and l + self.ring < self.pool.L:
+            # slot of layer l is free once this blend ran: refill it with l + ring
+            self.slot_free[l].record()
+            self._issue_copy(l + self.ring, after=self.slot_free[l])
 
     def step(self, suffix=None, logits_out: torch.Tensor | None = None,
              hook=None) -> torch.Tensor:
@@ -261,19 +314,13 @@ class SelectivePrefillEngine:
         C, N = self.C, pool.N
         if self.record_timeline:
             self._ev("step", 0, 0).record()
-        if self.pinned:
+        if self.pinned and self.n_segs and self.res < pool.L:
+            # the first `ring` streamed layers go out before anything else of
+            # the request (selection, embedding); the previous request's
+            # blends (which read the same slots) precede step_start
             self.step_start.record()
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_event(self.step_start)
-                cs = _dev.stream_handle(self.copy_stream)
-                for l in range(pool.L):
-                    d, s, b = self.copy_args[l]
-                    if self.record_timeline:
-                        self._ev("transfer", l, 0).record(self.copy_stream)
-                    _lib.call("ct_copy_ranges_h2d", d, s, b, C, cs)
-                    self.copy_done[l].record(self.copy_stream)
-                    if self.record_timeline:
-                        self._ev("transfer", l, 1).record(self.copy_stream)
+            for i, l in enumerate(range(self.res, min(pool.L, self.res + self.ring))):
+                self._issue_copy(l, after=self.step_start if i == 0 else None)
         if suffix is not None and self.S:
             self.tokens[self.n_rec:].copy_(suffix, non_blocking=True)
         m = self.meta

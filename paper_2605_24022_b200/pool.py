@@ -50,7 +50,12 @@ class SparseFetchPlan:
 class KvPool:
     """Importance-ordered pool of equal-geometry chunks."""
 
-    def __init__(self, chunks, rankings, location: str = "hbm", device=None):
+    def __init__(self, chunks, rankings, location: str = "hbm", device=None,
+                 resident_layers: int = 0):
+        """resident_layers (pinned pools): the first n layers' importance-
+        ordered rows are also kept in HBM, so a request's earliest layers --
+        whose transfer nothing can overlap -- read them in place (tiered
+        placement; the other layers stream over PCIe)."""
         if len(chunks) == 0 or len(chunks) != len(rankings):
             raise InvalidPlan("need one ranking per chunk")
         if location not in ("hbm", "pinned"):
@@ -98,11 +103,15 @@ class KvPool:
                     _lib.call("ct_gather_rows", _dev.ptr(src), _dev.ptr(perm), N,
                               self.row_bytes, _dev.ptr(tmp), _dev.stream_handle())
                     dev_img[ci, l, :, side].copy_(tmp)
+        self.resident_layers = 0 if location == "hbm" else max(0, min(int(resident_layers), L))
+        self.resident = None
         if location == "hbm":
             self.data = dev_img
         else:
             self.data = torch.empty(shape, dtype=self.dtype, pin_memory=True)
             self.data.copy_(dev_img)
+            if self.resident_layers:
+                self.resident = dev_img[:, :self.resident_layers].clone()
             del dev_img
         self._stats_lock = threading.Lock()
         self.io_stats = {"bytes_read": 0, "reads": 0}
@@ -125,6 +134,13 @@ class KvPool:
 
     def tail_ptr(self, c: int, l: int, k: int) -> int:
         return self.data.data_ptr() + self.offset_bytes(c, l, k)
+
+    def resident_tail_ptr(self, c: int, l: int, k: int) -> int:
+        """HBM address of a resident layer's keep tail (l < resident_layers)."""
+        if not 0 <= l < self.resident_layers:
+            raise InvalidParam(f"layer {l} is not HBM-resident")
+        R = self.resident_layers
+        return self.resident.data_ptr() + (((c * R + l) * self.N + k) * 2) * self.row_bytes
 
     # -- reference-shaped sparse API (ct/cachepool.py:409-481) ------------------
     def plan_sparse_fetch(self, chunk_id, layer: int, r: float) -> SparseFetchPlan:
