@@ -202,6 +202,62 @@ def cpu_sample(cfgname: str, seed: int = 0, rows: int = 32):
     return per_layer * c["layers"], desc
 
 
+def cfg1_end_to_end(repeats: int = 3) -> dict:
+    """Config 1 end to end on both sides: the 2-layer
+    toy model, 4 chunks x 512 tokens + 32 suffix, r = 0.15.  CPU = the oracle
+    port of the reference (rank_chunk x 4 + selective_prefill, float64 numpy,
+    the reference runs this config as-is); GPU = the drop-in API on host
+    inputs (rank_chunk x 4 + selective_prefill, fp32 mode, H2D/D2H included).
+    Best of `repeats`; the GPU logits are checked against the oracle's."""
+    import torch
+    import paper_2605_24022_b200 as ct
+    from oracle import cachetune_oracle as O
+    om = O.Model(O.ModelConfig(seed=0, n_layers=2))
+    rng = np.random.default_rng([0, 1])
+    toks = [rng.integers(0, 256, size=512) for _ in range(4)]
+    suffix = rng.integers(0, 256, size=32)
+    ochunks, chunks = [], []
+    for j, t in enumerate(toks):
+        kr, vs = O.encode_chunk_isolated(om, t)
+        ochunks.append((kr, vs, t))
+        chunks.append(ct.KvChunk(f"c{j}", tuple(ct.SeqTensor(k) for k in kr),
+                                 tuple(ct.SeqTensor(v) for v in vs), source_tokens=t))
+    gm = ct.GpuModel.from_reference(om, dtype=torch.float32)
+
+    # the reference's own semantics on both sides: PrefillResult with the
+    # attention record and the logits of every active row (ct/toymodel.py:223-311)
+    def cpu_once():
+        aggs = [O.rank_chunk(kr, vs)[2] for kr, vs, _ in ochunks]
+        return O.selective_prefill(om, ochunks, aggs, suffix, 0.15)
+
+    def gpu_once():
+        ranks = [ct.rank_chunk(c) for c in chunks]
+        res = ct.selective_prefill(gm, chunks, ranks, suffix, 0.15).to_host()
+        return res.logits
+
+    gpu_once()
+    torch.cuda.synchronize()
+    t_gpu, t_cpu = [], []
+    for _ in range(repeats):
+        t0 = time.perf_counter()
+        got = gpu_once()
+        t_gpu.append(time.perf_counter() - t0)
+    with all_host_threads():
+        for _ in range(repeats):
+            t0 = time.perf_counter()
+            want = cpu_once()
+            t_cpu.append(time.perf_counter() - t0)
+    err = O.normwise_rel(np.asarray(got, np.float64), want["logits"])
+    return {"workload": "config 1: 2-layer toy model (H=2, D=8), 4 chunks x 512 + 32 suffix, "
+                        "r = 0.15, rank_chunk x 4 + selective_prefill end to end",
+            "gpu_ms": min(t_gpu) * 1e3, "cpu_ms": min(t_cpu) * 1e3,
+            "cpu_kind": "port", "cpu_cores": cpu_threads(),
+            "speedup": min(t_cpu) / min(t_gpu), "logits_normwise_err": err,
+            "note": "wall clock, best of %d; both sides return the attention record and every "
+                    "active row's logits; GPU = drop-in API on host KvChunks (fp32 mode, copies "
+                    "included), a launch-bound toy shape" % repeats}
+
+
 def cpu_threads() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -297,6 +353,7 @@ def run_ours(args, rank, world, local_rank):
     from paper_2605_24022_b200 import _lib
     from paper_2605_24022_b200.pipeline import (FullPrefillEngine, KernelTimer,
                                                 SelectivePrefillEngine)
+    from paper_2605_24022_b200.offline import encode_and_rank, encode_batch
     from paper_2605_24022_b200.pool import KvPool
     from paper_2605_24022_b200.spectral import score_device, score_select_fast, selection_count
 
@@ -316,14 +373,32 @@ def run_ours(args, rank, world, local_rank):
     rng = np.random.default_rng([rank, 7])
     toks = [rng.integers(0, cfg.vocab_size, size=c["chunk_tokens"]) for _ in range(c["chunks"])]
     suffix = rng.integers(0, cfg.vocab_size, size=c["suffix"]).astype(np.int32)
-    chunks = [ct.encode_chunk_isolated(model, t, chunk_id=f"r{rank}c{j}")
-              for j, t in enumerate(toks)]
+    # offline stage: encode straight into the scorer's
+    # [C, L, N, Hkv, D] batch, score it, one permute launch builds the pool
+    ids = [f"r{rank}c{j}" for j in range(len(toks))]
+    keys, vals, chunks = encode_batch(model, toks, ids)  # warm-up + the batch buffers
     torch.cuda.synchronize()
+    e_enc = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e_enc[0].record()
+    encode_batch(model, toks, ids, out=(keys, vals))
+    e_enc[1].record()
+    torch.cuda.synchronize()
+    encode_ms = e_enc[0].elapsed_time(e_enc[1])
+    # the same with each chunk's exact scorer overlapped on a side stream
+    # (the scorer is FP-pipe bound, the encode tensor-pipe bound)
+    encode_and_rank(model, toks[:1], 0.5, "f64", ids[:1])  # warm-up of the side-stream path
+    torch.cuda.synchronize()
+    e_ov = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    e_ov[0].record()
+    ov = encode_and_rank(model, toks, 0.5, "f64", ids, out=(keys, vals))
+    e_ov[1].record()
+    torch.cuda.synchronize()
+    encode_rank_ms = e_ov[0].elapsed_time(e_ov[1])
+    ov_agg = ov[3]["agg_order"]
+    del ov
     log(f"[bench] model + {len(chunks)} encoded chunks in {time.time() - t0:.1f}s")
 
     # (1) scorer (offline stage): f64 exact mode over the request's chunks
-    keys = torch.stack([ch.keys for ch in chunks])
-    vals = torch.stack([ch.values for ch in chunks])
     sc_times = {}
     k_sel = selection_count(c["r"], c["chunk_tokens"])
     scorers = {"f64": lambda: score_device(keys, vals, 0.5, "f64", want_layer_order=False),
@@ -357,9 +432,30 @@ def run_ours(args, rank, world, local_rank):
             aggregate_order=agg_rows[j].cpu().numpy().astype(np.int64), alpha=0.5,
             n_tokens=n, device_aggregate=agg_rows[j]))
     scorer_bytes = keys.numel() * keys.element_size() * 2
-    del keys, vals
 
+    KvPool(chunks[:1], rankings[:1], "hbm", device=dev)  # warm-up
     pool_hbm = KvPool(chunks, rankings, "hbm", device=dev)
+    permute_ms = pool_hbm.permute_ms  # device time of the one permute launch
+    permute_bytes = 2 * scorer_bytes  # every K/V byte read once and written once
+    nch = len(chunks)
+    offline = {
+        "chunks": nch, "chunk_tokens": c["chunk_tokens"],
+        "encode_ms_per_chunk": encode_ms / nch,
+        "score_f64_ms_per_chunk": None, "score_fast_ms_per_chunk": None,
+        "encode_rank_overlapped_ms_per_chunk": encode_rank_ms / nch,
+        "permute_ms_per_chunk": permute_ms / nch,
+        "permute_launches": pool_hbm.permute_launches,
+        "permute": {"bound": "hbm", "bytes": permute_bytes,
+                    "achieved": permute_bytes / (permute_ms * 1e-3) / 1e9,
+                    "peak": peaks["hbm"], "unit": "GB/s",
+                    "frac": permute_bytes / (permute_ms * 1e-3) / 1e9 / peaks["hbm"]},
+        "overlapped_orders_equal": bool(torch.equal(ov_agg, agg_rows)),
+        "note": "encode writes K/V into the [C, L, N, Hkv, D] scorer batch; one scorer launch "
+                "set; one ct_pool_permute launch writes the importance-ordered pool.  "
+                "encode_rank_overlapped = encode with each chunk's exact (f64) scorer on a side "
+                "stream behind it (offline.encode_and_rank)",
+    }
+    del keys, vals
     pool_pin = KvPool(chunks, rankings, "pinned", device=dev,
                       resident_layers=args.resident_layers)
     del chunks
@@ -469,6 +565,8 @@ def run_ours(args, rank, world, local_rank):
     scfast = allmax(sc_times["fast"])
     if rank != 0:
         return
+    offline["score_f64_ms_per_chunk"] = sc64 / nch
+    offline["score_fast_ms_per_chunk"] = scfast / nch
 
     L = cfg.n_layers
     att_flops = eng.attention_flops_per_layer()
@@ -511,6 +609,10 @@ def run_ours(args, rank, world, local_rank):
             sec, desc = cpu_sample(args.config, rows=args.cpu_rows)
         cpu = {"value": 1.0 / sec, "unit": "requests/s", "cores": cpu_threads(), "kind": "port",
                "sample": desc, "host": host_info()}
+        try:
+            cpu["cfg1_end_to_end"] = cfg1_end_to_end()
+        except Exception as e:  # reported, never silently dropped
+            cpu["cfg1_end_to_end"] = {"error": f"{type(e).__name__}: {e}"}
     line = {
         "metric": METRIC, "value": value, "unit": "requests/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
@@ -564,6 +666,7 @@ def run_ours(args, rank, world, local_rank):
                         "(window tokens re-scored in float64); orders exact at k",
                 "traffic": ncu_traffic("fs_energy_kernel", args.config)},
         },
+        "offline": offline,
         "step_tflops": step_flops / (p50 * 1e-3) / 1e12,
         "sparse_h2d": {
             "bound": "pcie", "bytes_per_request": e2e_h2d, "copy_engine_ms": h2d_ms,

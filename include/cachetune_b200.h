@@ -228,6 +228,18 @@ int ct_scatter_rows(const void* src, const int32_t* idx, int64_t n,
 int ct_gather_rows(const void* src, const int32_t* idx, int64_t n,
                    int64_t row_bytes, void* dst, void* stream);
 
+
+/* Importance-ordered pool image, the offline stage's last step (layout of
+ * pool.py; replaces the reference's per-token CTKV writes,
+ * ct/cachepool.py:167-230 + the keep-set ranges of :409-435):
+ *   dst[((c*L + l)*N + p)*2 + side] (row_bytes each) =
+ *       (side ? values : keys)[c*ld_chunk + l*ld_layer + order[c*N + p]*ld_token]
+ * Strides in BYTES, multiples of 4 (16-byte rows and strides take the
+ * vector path).  One launch for all C chunks. */
+int ct_pool_permute(const void* keys, const void* values, int C, int L, int N,
+                    int64_t ld_token, int64_t ld_layer, int64_t ld_chunk,
+                    int64_t row_bytes, const int32_t* order, void* dst, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* (4) selective-recompute attention -- ct/toymodel.py:176-183.
  * Queries q [A][Hq][D] at global positions q_pos[a] (ascending not

@@ -87,6 +87,8 @@ _SIGS = {
                                     c_void_p, c_void_p, c_int, c_int64, c_void_p, c_void_p]),
     "ct_scatter_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
     "ct_gather_rows": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_void_p]),
+    "ct_pool_permute": (c_int, [c_void_p, c_void_p, c_int, c_int, c_int, c_int64, c_int64,
+                                c_int64, c_int64, c_void_p, c_void_p, c_void_p]),
     "ct_attention_workspace_bytes": (c_size_t, [c_int64, c_int64, c_int64, c_int64, c_int64,
                                                 c_int]),
     "ct_selective_attention": (c_int, [c_void_p, c_void_p, c_int64, c_int64, c_void_p,

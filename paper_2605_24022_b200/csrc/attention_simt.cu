@@ -387,8 +387,11 @@ int attention_decode(const void* q, const int32_t* q_pos, int64_t A, int64_t Hq,
       crs, (float)(scale * 1.4426950408889634), (int)keys, (float*)workspace);
   int rc = check_launch("attention_decode_partial");
   if (rc) return rc;
-  attention_decode_combine<TO><<<dim3((unsigned)R, (unsigned)Hkv), DEC_THREADS,
-                                 (size_t)splits * sizeof(float), st>>>(
+  // the weights array is padded to whole 16-byte vectors plus one: the
+  // compiler reads the split tail with 16-byte shared loads (compute-sanitizer
+  // memcheck flagged the over-read past an exact-size allocation)
+  const size_t cw_bytes = (size_t)((splits + 3) / 4 * 4 + 4) * sizeof(float);
+  attention_decode_combine<TO><<<dim3((unsigned)R, (unsigned)Hkv), DEC_THREADS, cw_bytes, st>>>(
       (const float*)workspace, (int)A, (int)Hq, (int)Hkv, (int)D, (int)splits, (TO*)out);
   return check_launch("attention_decode_combine");
 }

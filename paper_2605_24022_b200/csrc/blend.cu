@@ -396,6 +396,56 @@ __global__ void rows_copy_kernel(const uint32_t* __restrict__ src, const int32_t
   }
 }
 
+
+// Importance-ordered pool image (offline stage): one warp per destination
+// (chunk, layer, rank p) moves the K row then the V row of token order[c][p].
+// W = uint4 (16-byte rows) or uint32_t; VPL > 0: the row is VPL vectors per
+// lane and all 2*VPL loads are issued before the streaming stores (16 KiB in
+// flight per warp-row at VPL = 4), VPL = 0: generic lane loop.  Every byte
+// crosses HBM once in each direction.  dst[((c L + l) N + p) 2 + side][row].
+template <typename W>
+__device__ __forceinline__ W ld_once(const W* p) { return __ldg(p); }
+template <>
+__device__ __forceinline__ uint4 ld_once<uint4>(const uint4* p) { return ldg_stream(p); }
+
+template <typename W, int VPL>
+__global__ void __launch_bounds__(256)
+pool_permute_kernel(const W* __restrict__ keys, const W* __restrict__ values, int C, int L, int N,
+                    int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int vec,
+                    const int32_t* __restrict__ order, W* __restrict__ dst) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t total = (int64_t)C * L * N;
+  for (int64_t u = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5); u < total;
+       u += warps) {
+    const int p = (int)(u % N);
+    const int64_t cl = u / N;
+    const int l = (int)(cl % L), c = (int)(cl / L);
+    const int64_t src =
+        c * ld_chunk + l * ld_layer + (int64_t)__ldg(order + (int64_t)c * N + p) * ld_token;
+    W* out = dst + u * 2 * vec;
+    if constexpr (VPL > 0) {
+      W k[VPL], v[VPL];
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        k[i] = ld_once(keys + src + lane + 32 * i);
+        v[i] = ld_once(values + src + lane + 32 * i);
+      }
+#pragma unroll
+      for (int i = 0; i < VPL; ++i) {
+        __stcs(out + lane + 32 * i, k[i]);
+        __stcs(out + vec + lane + 32 * i, v[i]);
+      }
+    } else {
+      for (int w = lane; w < vec; w += 32) {
+        const W k = ld_once(keys + src + w), v = ld_once(values + src + w);
+        __stcs(out + w, k);
+        __stcs(out + vec + w, v);
+      }
+    }
+  }
+}
+
 static unsigned grid_for(int64_t units, int threads) {
   int64_t b = (units + threads - 1) / threads;
   const int64_t cap = 148 * 32;
@@ -598,4 +648,43 @@ extern "C" int ct_gather_rows(const void* src, const int32_t* idx, int64_t n, in
   rows_copy_kernel<<<grid_for(n * words, 256), 256, 0, (cudaStream_t)stream>>>(
       (const uint32_t*)src, idx, n, words, (uint32_t*)dst, false);
   return check_launch("rows_copy_kernel");
+}
+
+extern "C" int ct_pool_permute(const void* keys, const void* values, int C, int L, int N,
+                               int64_t ld_token, int64_t ld_layer, int64_t ld_chunk,
+                               int64_t row_bytes, const int32_t* order, void* dst, void* stream) {
+  if (C < 0 || L < 0 || N < 0) return fail(CT_ERR_SHAPE, "ct_pool_permute: negative geometry");
+  if (row_bytes <= 0 || row_bytes % 4 || ld_token % 4 || ld_layer % 4 || ld_chunk % 4)
+    return fail(CT_ERR_PARAM, "ct_pool_permute: row bytes and strides must be multiples of 4");
+  if (ld_token < row_bytes) return fail(CT_ERR_SHAPE, "ct_pool_permute: token stride < row bytes");
+  if (((uintptr_t)keys | (uintptr_t)values | (uintptr_t)dst) & 3)
+    return fail(CT_ERR_PARAM, "ct_pool_permute: pointers must be 4-byte aligned");
+  if ((int64_t)C * L * N == 0) return CT_OK;
+  if (!keys || !values || !order || !dst) return fail(CT_ERR_PARAM, "ct_pool_permute: null pointer");
+  const int64_t warps = (int64_t)C * L * N;
+  int64_t blocks = (warps + 7) / 8;
+  const int64_t cap = 148 * 8;
+  if (blocks > cap) blocks = cap;
+  cudaStream_t st = (cudaStream_t)stream;
+  const bool v16 = row_bytes % 16 == 0 && ld_token % 16 == 0 && ld_layer % 16 == 0 &&
+                   ld_chunk % 16 == 0 && !(((uintptr_t)keys | (uintptr_t)values | (uintptr_t)dst) & 15);
+  if (v16) {
+    const int vec = (int)(row_bytes / 16);
+    auto args = [&](auto kern) {
+      kern<<<(unsigned)blocks, 256, 0, st>>>((const uint4*)keys, (const uint4*)values, C, L, N,
+                                             ld_token / 16, ld_layer / 16, ld_chunk / 16, vec,
+                                             order, (uint4*)dst);
+    };
+    if (vec == 128)
+      args(pool_permute_kernel<uint4, 4>);
+    else if (vec == 256)
+      args(pool_permute_kernel<uint4, 8>);
+    else
+      args(pool_permute_kernel<uint4, 0>);
+  } else {
+    pool_permute_kernel<uint32_t, 0><<<(unsigned)blocks, 256, 0, st>>>(
+        (const uint32_t*)keys, (const uint32_t*)values, C, L, N, ld_token / 4, ld_layer / 4,
+        ld_chunk / 4, (int)(row_bytes / 4), order, (uint32_t*)dst);
+  }
+  return check_launch("pool_permute_kernel");
 }

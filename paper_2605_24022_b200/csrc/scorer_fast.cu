@@ -215,16 +215,38 @@ __device__ __forceinline__ cf load_pair<float>(const float* p) {
   return __ldg(reinterpret_cast<const float2*>(p));
 }
 
+__device__ __forceinline__ void cp_async16(const void* dst_smem, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   (uint32_t)__cvta_generic_to_shared(dst_smem)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ cf unpack_bf16x2(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+// bf16 inputs with 16-byte aligned rows: a batch's 16 lanes x 2048 tokens
+// (32 B per token, 64 KiB) are staged in shared memory by cp.async one batch
+// ahead, so step 1 reads shared memory while the next batch is in flight.
+constexpr size_t STAGE_BYTES = (size_t)N * SIG_PER_BATCH * 4;
+
 // grid: x = lane group (SIG_PER_CTA signals), y = tensor (0 K, 1 V), z = c*L + l.
 // partial[((c*L + l)*2 + tensor)*G + group][N] f32 (unnormalised |y|^2, x N^2)
-template <typename IN>
+template <typename IN, bool STAGE, bool LB>
 __global__ void __launch_bounds__(THREADS, 1)
 fs_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int L,
                  int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, int cutoff, int high,
                  const float2* __restrict__ tw, int groups, float* __restrict__ partial) {
+  static_assert(!STAGE || sizeof(IN) == 2, "staging is for bf16 rows");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cf* xb = reinterpret_cast<cf*>(smem_raw);                  // [8][32][64]
   cf* T = xb + SIG_PER_BATCH * 32 * 64;                       // W_2048^m, m < 2048
+  uint32_t* stg = reinterpret_cast<uint32_t*>(T + N);         // [N][8] bf16x2 (STAGE)
   const int t = threadIdx.x, s = t & 7, q = t >> 3;
   const int tensor = blockIdx.y, group = blockIdx.x;
   const int c = blockIdx.z / L, l = blockIdx.z % L;
@@ -237,18 +259,42 @@ fs_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int
   float acc[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc[i] = 0.f;
+  // batch b's 16 lanes of every token: thread t moves 16-byte halves (t & 1)
+  // of token rows t/2 + 128 i (sector-complete 32-byte row pieces per pair)
+  auto prefetch = [&](int b) {
+    const IN* src = base + b * SIG_PER_BATCH * 2 + (t & 1) * 8 + (int64_t)(t >> 1) * ld_token;
+    uint32_t* dst = stg + (t >> 1) * SIG_PER_BATCH + (t & 1) * 4;
+    const int64_t step = (int64_t)(THREADS / 2) * ld_token;
+#pragma unroll 1
+    for (int i = 0; i < N / (THREADS / 2); ++i) {
+      cp_async16(dst, src);
+      src += step;
+      dst += (THREADS / 2) * SIG_PER_BATCH;
+    }
+    cp_async_commit();
+  };
+  if constexpr (STAGE) prefetch(0);
   __syncthreads();
 
 #pragma unroll 1
   for (int b = 0; b < BATCHES; ++b) {
     const IN* sig = base + (b * SIG_PER_BATCH + s) * 2;
+    if constexpr (STAGE) {
+      cp_async_wait_all();
+      __syncthreads();
+    }
     // ---- step 1: 32-point DFT over n1 of tokens n2 + 64 n1, twiddle, exchange
 #pragma unroll
     for (int jb = 0; jb < 2; ++jb) {
       const int n2 = q + 32 * jb;
       cf v[32];
 #pragma unroll
-      for (int n1 = 0; n1 < 32; ++n1) v[n1] = load_pair<IN>(sig + (int64_t)(n2 + 64 * n1) * ld_token);
+      for (int n1 = 0; n1 < 32; ++n1) {
+        if constexpr (STAGE)
+          v[n1] = unpack_bf16x2(stg[(n2 + 64 * n1) * SIG_PER_BATCH + s]);
+        else
+          v[n1] = load_pair<IN>(sig + (int64_t)(n2 + 64 * n1) * ld_token);
+      }
       fwd<32>(v);
 #pragma unroll
       for (int p = 0; p < 32; ++p) {
@@ -257,21 +303,56 @@ fs_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int
       }
     }
     __syncthreads();
+    // every thread is past its staged reads: the next batch streams in
+    // behind steps 2 and 3
+    if constexpr (STAGE) {
+      if (b + 1 < BATCHES) prefetch(b + 1);
+    }
     // ---- step 2: per k1 = q: 64-point DFT over n2, band mask, inverse, twiddle
     {
       const int k1 = q;
       cf u[64];
 #pragma unroll
       for (int n2 = 0; n2 < 64; ++n2) u[n2] = xb[xidx(s, k1, n2)];
-      fwd<64>(u);
+      if constexpr (LB) {
+        // default band (low, cutoff N/4): the last forward radix-4 stage
+        // holds the top digit of k2 at position p & 3, and digits 1 and 2
+        // (k2 in [16, 48)) are always cut, so that stage, the mask and the
+        // first inverse stage fuse into 10 complex adds per group instead
+        // of 16 -- the same operations on the surviving values as the
+        // generic path below (bitwise the same energies)
+        dif_stage<64, 64, -1>(u);
+        dif_twiddle<64, 64, -1>(u);
+        dif_stage<64, 16, -1>(u);
+        dif_twiddle<64, 16, -1>(u);
 #pragma unroll
-      for (int p = 0; p < 64; ++p) {
-        const int k = k1 + 32 * digrev<64>(p);
-        const int kk = min(k, N - k);
-        const bool keep = high ? kk >= cutoff : kk < cutoff;
-        if (!keep) u[p] = make_float2(0.f, 0.f);
+        for (int g = 0; g < 64; g += 4) {
+          const cf a = u[g], b = u[g + 1], c = u[g + 2], d = u[g + 3];
+          const cf t0 = a + c, t1 = a - c, t2 = b + d;
+          const cf x0 = t0 + t2;
+          cf x3 = t1 - mul_i<-1>(b - d);
+          if (g == 0 && k1 == 0) x3 = make_float2(0.f, 0.f);  // k = 3N/4 is cut
+          const cf t3 = mul_i<1>(make_float2(0.f, 0.f) - x3);
+          u[g] = x0 + x3;
+          u[g + 2] = x0 - x3;
+          u[g + 1] = x0 + t3;
+          u[g + 3] = x0 - t3;
+        }
+        dit_twiddle<64, 16, 1>(u);
+        dit_stage<64, 16, 1>(u);
+        dit_twiddle<64, 64, 1>(u);
+        dit_stage<64, 64, 1>(u);
+      } else {
+        fwd<64>(u);
+#pragma unroll
+        for (int p = 0; p < 64; ++p) {
+          const int k = k1 + 32 * digrev<64>(p);
+          const int kk = min(k, N - k);
+          const bool keep = high ? kk >= cutoff : kk < cutoff;
+          if (!keep) u[p] = make_float2(0.f, 0.f);
+        }
+        inv<64>(u);
       }
-      inv<64>(u);
       // this thread's row of the buffer is read and written by it alone
 #pragma unroll
       for (int n2 = 0; n2 < 64; ++n2) xb[xidx(s, k1, n2)] = cmulc(u[n2], T[(n2 * k1) & (N - 1)]);
@@ -585,14 +666,26 @@ extern "C" int ct_score_select_fast(const void* keys, const void* values, int dt
   if ((rc = check_launch("fs_twiddle"))) return rc;
   const size_t smem = (size_t)fs::SIG_PER_BATCH * 32 * 64 * sizeof(fs::cf) + fs::N * sizeof(fs::cf);
   dim3 grid((unsigned)groups, 2, (unsigned)(C * L));
-  if (dtype == CT_BF16) {
-    auto kern = fs::fs_energy_kernel<__nv_bfloat16>;
+  const bool aligned16 = !(((uintptr_t)keys | (uintptr_t)values) & 15) && ld_token % 8 == 0 &&
+                         ld_layer % 8 == 0 && ld_chunk % 8 == 0;
+  const bool lb = band == 0 && cutoff == fs::N / 4;
+  if (dtype == CT_BF16 && aligned16) {
+    auto kern = lb ? fs::fs_energy_kernel<__nv_bfloat16, true, true>
+                   : fs::fs_energy_kernel<__nv_bfloat16, true, false>;
+    const size_t smem_st = smem + fs::STAGE_BYTES;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_st));
+    kern<<<grid, fs::THREADS, smem_st, st>>>((const __nv_bfloat16*)keys,
+                                             (const __nv_bfloat16*)values, (int)L, ld_token,
+                                             ld_layer, ld_chunk, (int)cutoff, band, tw, groups,
+                                             partial);
+  } else if (dtype == CT_BF16) {
+    auto kern = fs::fs_energy_kernel<__nv_bfloat16, false, false>;
     CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, fs::THREADS, smem, st>>>((const __nv_bfloat16*)keys, (const __nv_bfloat16*)values,
                                           (int)L, ld_token, ld_layer, ld_chunk, (int)cutoff, band,
                                           tw, groups, partial);
   } else {
-    auto kern = fs::fs_energy_kernel<float>;
+    auto kern = fs::fs_energy_kernel<float, false, false>;
     CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, fs::THREADS, smem, st>>>((const float*)keys, (const float*)values, (int)L,
                                           ld_token, ld_layer, ld_chunk, (int)cutoff, band, tw,

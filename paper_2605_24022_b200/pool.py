@@ -70,6 +70,8 @@ class KvPool:
                 raise InvalidPlan("ranking/chunk token counts disagree")
         self.location = location
         self.device = torch.device(device)
+        if self.device.type == "cuda" and self.device.index is None:
+            self.device = torch.device("cuda", torch.cuda.current_device())
         self.dtype = c0.keys.dtype
         self.C, self.L, self.N, self.H, self.D = len(chunks), L, N, H, D
         self.chunk_ids = [c.chunk_id for c in chunks]
@@ -95,14 +97,7 @@ class KvPool:
                                      for c in chunks])
         shape = (self.C, L, N, 2, H, D)
         dev_img = torch.empty(shape, dtype=self.dtype, device=self.device)
-        tmp = torch.empty((N, H, D), dtype=self.dtype, device=self.device)
-        for ci, c in enumerate(chunks):   # offline: permute rows into importance order
-            perm = self.agg[ci]
-            for l in range(L):
-                for side, src in ((0, c.keys[l]), (1, c.values[l])):
-                    _lib.call("ct_gather_rows", _dev.ptr(src), _dev.ptr(perm), N,
-                              self.row_bytes, _dev.ptr(tmp), _dev.stream_handle())
-                    dev_img[ci, l, :, side].copy_(tmp)
+        self._permute(chunks, dev_img)
         self.resident_layers = 0 if location == "hbm" else max(0, min(int(resident_layers), L))
         self.resident = None
         if location == "hbm":
@@ -115,6 +110,46 @@ class KvPool:
             del dev_img
         self._stats_lock = threading.Lock()
         self.io_stats = {"bytes_read": 0, "reads": 0}
+
+    def _permute(self, chunks, dev_img) -> None:
+        """Offline: rows into importance order with ct_pool_permute -- one
+        launch for all chunks when they are slices of one [C, L, N, H, D]
+        batch (the offline stage's layout), else one launch per chunk."""
+        L, N = self.L, self.N
+        ks, vs = [c.keys for c in chunks], [c.values for c in chunks]
+        for t in ks + vs:
+            if t.device != self.device or not t.is_contiguous() or t.dtype != self.dtype:
+                raise InvalidParam("pool chunks must be contiguous tensors of one dtype on the "
+                                   "pool's device")
+        row = self.row_bytes
+        st = _dev.stream_handle()
+
+        def uniform(ts):
+            if len(ts) < 2:
+                return 0
+            d = ts[1].data_ptr() - ts[0].data_ptr()
+            ok = d > 0 and all(b.data_ptr() - a.data_ptr() == d for a, b in zip(ts, ts[1:]))
+            return d if ok else 0
+        dk, dv = uniform(ks), uniform(vs)
+        # chunk c's rows live at base + c * ld_chunk exactly when the spacing
+        # of the chunks' own data pointers is uniform (checked above)
+        groups = ([(0, self.C, dk)] if dk and dk == dv
+                  else [(ci, 1, L * N * row) for ci in range(self.C)])
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        ev[0].record()
+        for c0, nc, ld_chunk in groups:
+            _lib.call("ct_pool_permute", _dev.ptr(ks[c0]), _dev.ptr(vs[c0]), nc, L, N, row,
+                      N * row, ld_chunk, row, _dev.ptr(self.agg[c0]), _dev.ptr(dev_img[c0]), st)
+        ev[1].record()
+        self.permute_launches = len(groups)
+        self._permute_events = ev
+
+    @property
+    def permute_ms(self) -> float:
+        """Device time of the offline permute launches (synchronises)."""
+        ev = self._permute_events
+        ev[1].synchronize()
+        return ev[0].elapsed_time(ev[1])
 
     # -- geometry ----------------------------------------------------------
     @property

@@ -330,8 +330,12 @@ def full_prefill(model, tokens: Sequence[int], *, record_attention=None,
 
 
 def encode_chunk_isolated(model, tokens: Sequence[int], chunk_id: str = "chunk", *,
-                          dtype=None) -> DeviceChunk:
-    """Forward the chunk alone at local positions; keep pre-RoPE K (ct/toymodel.py:208-220)."""
+                          dtype=None, out=None) -> DeviceChunk:
+    """Forward the chunk alone at local positions; keep pre-RoPE K (ct/toymodel.py:208-220).
+
+    out=(keys, values): contiguous [L, N, Hkv, D] device tensors of the model
+    dtype the layers write into (e.g. one chunk's slice of the offline stage's
+    [C, L, N, Hkv, D] scorer batch), instead of fresh allocations."""
     g = as_gpu_model(model, dtype)
     toks = np.asarray(tokens, dtype=np.int64)
     _check_tokens(g, toks)
@@ -339,8 +343,15 @@ def encode_chunk_isolated(model, tokens: Sequence[int], chunk_id: str = "chunk",
     dev = g.device
     n = toks.size
     shape = (cfg.n_layers, n, cfg.kv_heads, cfg.head_dim)
-    keys = torch.empty(shape, dtype=g.dtype, device=dev)
-    vals = torch.empty(shape, dtype=g.dtype, device=dev)
+    if out is None:
+        keys = torch.empty(shape, dtype=g.dtype, device=dev)
+        vals = torch.empty(shape, dtype=g.dtype, device=dev)
+    else:
+        keys, vals = out
+        for t in (keys, vals):
+            if tuple(t.shape) != shape or t.dtype != g.dtype or not t.is_contiguous() \
+                    or t.device != torch.device(dev):
+                raise ShapeError(f"out tensors must be contiguous {shape} {g.dtype} on {dev}")
     krot = torch.empty(shape[1:], dtype=g.dtype, device=dev)
     caches = [(krot, vals[l]) for l in range(cfg.n_layers)]
     tok_d = torch.as_tensor(toks.astype(np.int32), device=dev)

@@ -110,12 +110,15 @@ def _as_device_kv(keys, values):
 
 
 def score_device(keys: torch.Tensor, values: torch.Tensor, alpha: float = DEFAULT_ALPHA,
-                 precision: str = "f64", want_layer_order: bool = True, band: str = "low"):
+                 precision: str = "f64", want_layer_order: bool = True, band: str = "low",
+                 out: dict | None = None):
     """Score C chunks on the device (band "low", or "high" = ct/spectral.py:47-54).
 
     keys/values: [C, L, N, H, D] (or [L, N, H, D]) f32/bf16 CUDA tensors.
     Returns dict of device tensors: layer_scores [C,L,N] f64, agg [C,N] f64,
-    layer_order [C,L,N] int32 (optional), agg_order [C,N] int32."""
+    layer_order [C,L,N] int32 (optional), agg_order [C,N] int32.  `out`: the
+    same dict of caller-allocated contiguous tensors to write into (e.g. one
+    chunk's slices of a batch result)."""
     _check_alpha(alpha)
     if band not in ("low", "high"):
         raise InvalidParam(f"band must be 'low' or 'high', got {band!r}")
@@ -131,13 +134,20 @@ def score_device(keys: torch.Tensor, values: torch.Tensor, alpha: float = DEFAUL
     dev = keys.device
     cutoff = cutoff_index(alpha, N // 2 + 1)
     prec = _lib.CT_F64 if precision == "f64" else _lib.CT_F32
-    out = {
-        "layer_scores": torch.empty((C, L, N), dtype=torch.float64, device=dev),
-        "agg": torch.empty((C, N), dtype=torch.float64, device=dev),
-        "agg_order": torch.empty((C, N), dtype=torch.int32, device=dev),
-        "layer_order": (torch.empty((C, L, N), dtype=torch.int32, device=dev)
-                        if want_layer_order else None),
-    }
+    shapes = {"layer_scores": ((C, L, N), torch.float64), "agg": ((C, N), torch.float64),
+              "agg_order": ((C, N), torch.int32), "layer_order": ((C, L, N), torch.int32)}
+    if out is None:
+        out = {k: torch.empty(sh, dtype=dt, device=dev) for k, (sh, dt) in shapes.items()}
+        if not want_layer_order:
+            out["layer_order"] = None
+    else:
+        for k, (sh, dt) in shapes.items():
+            t = out.get(k)
+            if t is None and k == "layer_order" and not want_layer_order:
+                continue
+            if t is None or tuple(t.shape) != sh or t.dtype != dt or not t.is_contiguous() \
+                    or t.device != dev:
+                raise ShapeError(f"out[{k!r}] must be a contiguous {sh} {dt} tensor on {dev}")
     lib = _lib.load()
     wsb = lib.ct_score_workspace_bytes(C, L, N, lanes, prec)
     ws = _dev.workspace(wsb, "score")

@@ -139,7 +139,8 @@ def test_offline_prepare_pool_and_ctkv_export(ct, tmp_path):
     toks = [rng.integers(0, 256, size=256) for _ in range(3)]
     timings = {}
     pool = prepare_pool(om, toks, location="pinned", ctkv_dir=tmp_path, timings=timings)
-    assert set(timings) == {"encode_ms", "rank_ms", "pool_ms"}
+    assert {"encode_ms", "rank_ms", "pool_ms"} <= set(timings)
+    assert timings["permute_launches"] == 1  # the batch layout: one pool_permute launch
     for i in range(3):
         chunk, rk = ctkv.read_ctkv((tmp_path / f"chunk{i}.ctkv").read_bytes(), f"chunk{i}")
         assert np.array_equal(rk.aggregate_order, pool.agg[i].cpu().numpy())
@@ -245,3 +246,68 @@ def test_ctkv_pool_without_tokens_is_fetch_only(ct):
     assert ok.has_tokens == [True, True]
     SelectivePrefillEngine(m, ok, 0.15, 8).step(
         torch.zeros(8, dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_pool_permute_batch_and_per_chunk_bit_identical(ct, dtype):
+    """ct_pool_permute (offline stage): the importance-ordered image equals
+    torch indexing of the chunks' K/V by their aggregate orders, bit for bit,
+    whether the chunks are slices of one batch (one launch) or separate
+    allocations (one launch per chunk)."""
+    import torch
+    from paper_2605_24022_b200.kvcore import DeviceChunk
+    from paper_2605_24022_b200.pool import KvPool
+    torch.manual_seed(0)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    C, L, N, H, D = 3, 4, 200, 2, 64
+    keys = torch.randn(C, L, N, H, D, device="cuda").to(tdt)
+    vals = torch.randn(C, L, N, H, D, device="cuda").to(tdt)
+    orders = [np.random.default_rng(i).permutation(N) for i in range(C)]
+    ranks = [ct.ImportanceRanking(per_layer_scores=np.zeros((L, N)),
+                                  per_layer_order=np.tile(np.arange(N), (L, 1)),
+                                  aggregate_order=o, alpha=0.5, n_tokens=N) for o in orders]
+    want = torch.stack([torch.stack([keys[c][:, torch.as_tensor(orders[c], device="cuda")],
+                                     vals[c][:, torch.as_tensor(orders[c], device="cuda")]],
+                                    dim=2) for c in range(C)])
+    batch = [DeviceChunk(f"c{c}", keys[c], vals[c]) for c in range(C)]
+    pool = KvPool(batch, ranks, "hbm")
+    assert pool.permute_launches == 1
+    assert torch.equal(pool.data, want)
+    sep = [DeviceChunk(f"c{c}", keys[c].clone(), vals[c].clone()) for c in range(C)]
+    pool2 = KvPool(sep, ranks, "pinned")
+    assert pool2.permute_launches in (1, C)
+    assert torch.equal(pool2.data.cuda(), want)
+
+
+def test_pool_permute_rejects_bad_geometry(ct):
+    """Validation happens before any launch (no pointer is dereferenced)."""
+    from paper_2605_24022_b200 import _lib
+    with pytest.raises(ct.InvalidParam):   # row bytes not a multiple of 4
+        _lib.call("ct_pool_permute", 16, 16, 1, 1, 1, 8, 8, 8, 6, 16, 16, None)
+    with pytest.raises(ct.InvalidParam):   # misaligned pointer
+        _lib.call("ct_pool_permute", 18, 16, 1, 1, 1, 8, 8, 8, 8, 16, 16, None)
+    with pytest.raises(ct.ShapeError):     # rows overlap
+        _lib.call("ct_pool_permute", 16, 16, 1, 1, 1, 4, 8, 8, 8, 16, 16, None)
+
+
+def test_offline_overlapped_scoring_bit_identical(ct):
+    """encode_and_rank (chunk c scored on a side stream while chunk c+1 is
+    encoded) == encode_batch then one batched score_device, bit for bit, and
+    the pools built both ways are identical."""
+    import torch
+    from paper_2605_24022_b200.offline import encode_and_rank, encode_batch, prepare_pool
+    from paper_2605_24022_b200.spectral import score_device
+    cfg = ct.ModelConfig.llama3_8b(n_layers=2, vocab_size=1024, seed=8)
+    model = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(3)
+    toks = [rng.integers(0, 1024, size=2048) for _ in range(3)]
+    k1, v1, _, s1 = encode_and_rank(model, toks)
+    k2, v2, _ = encode_batch(model, toks)
+    s2 = score_device(k2, v2, 0.5, "f64", want_layer_order=True)
+    assert torch.equal(k1, k2) and torch.equal(v1, v2)
+    for key in ("layer_scores", "agg", "agg_order", "layer_order"):
+        assert torch.equal(s1[key], s2[key]), key
+    t1, t2 = {}, {}
+    p1 = prepare_pool(model, toks, location="hbm", timings=t1)
+    p2 = prepare_pool(model, toks, location="hbm", timings=t2, overlap=False)
+    assert torch.equal(p1.data, p2.data) and torch.equal(p1.agg, p2.agg)

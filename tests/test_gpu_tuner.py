@@ -1,0 +1,57 @@
+"""B200 refit of the adaptive-ratio tuner (ct/scheduler.py:207-237 with the
+cost model of :62-79 refit to this GPU): profile_b200 / measure_h2d_per_token
+fit t_c, t_i, t_o from real engine steps and copy-engine transfers, and
+calibrate() driven by make_gpu_evaluator (real TTFTs of a pinned-pool
+selective prefill) lands on the grid optimum of the same evaluator."""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def setup():
+    import torch
+    import paper_2605_24022_b200 as ct
+    from paper_2605_24022_b200.offline import prepare_pool
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    cfg = ct.ModelConfig.llama3_8b(n_layers=4, vocab_size=4096, seed=5)
+    model = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
+    rng = np.random.default_rng(11)
+    toks = [rng.integers(0, cfg.vocab_size, size=2048) for _ in range(8)]
+    pool = prepare_pool(model, toks, location="pinned")
+    return model, pool
+
+
+def test_profile_b200_fits_positive_rates(setup):
+    from paper_2605_24022_b200 import scheduler
+    model, pool = setup
+    prof = scheduler.profile_b200(model, pool)
+    assert prof.t_c > 0 and prof.t_i > 0 and prof.t_o >= 0
+    # t_i is copy-engine seconds per kept token per layer: K + V rows
+    gbs = 2 * pool.row_bytes / prof.t_i / 1e9
+    assert 5.0 < gbs < 80.0, f"implausible pinned H2D rate {gbs:.1f} GB/s"
+    # the roofline prior is a ratio inside the search interval
+    r0 = scheduler.roofline_r0(prof, scheduler.SearchConfig(r_min=0.05, r_max=0.5))
+    assert 0.05 <= r0 <= 0.5
+
+
+def test_calibrate_with_gpu_evaluator_matches_grid_optimum(setup):
+    from paper_2605_24022_b200 import scheduler
+    model, pool = setup
+    prof = scheduler.profile_b200(model, pool)
+    scfg = scheduler.SearchConfig(r_min=0.05, r_max=0.5, epsilon=0.02)
+    ev = scheduler.make_gpu_evaluator(model, pool, repeats=3)
+    rep = scheduler.calibrate(None, None, ev, ["request-0"], scfg, profile=prof)
+    assert scfg.r_min <= rep.r_star <= scfg.r_max
+    assert 2 <= rep.eval_count <= scheduler.gss_eval_budget(scfg)
+    grid = np.round(np.arange(0.05, 0.5001, 0.05), 4)
+    ttft = {float(r): ev("request-0", float(r)) for r in grid}
+    best = min(ttft.values())
+    got = ev("request-0", rep.r_star)
+    # the golden-section pick is within 10 % of the best grid ratio's TTFT
+    assert got <= 1.10 * best, (rep.r_star, got, ttft)
