@@ -692,7 +692,7 @@ def run_ours(args, rank, world, local_rank):
         "clocks": clk.summary(),
         "cpu_baseline": cpu,
     }
-    print(json.dumps(line), flush=True)
+    return line
 
 
 def run_batch(args, rank, world, local_rank):
@@ -848,6 +848,48 @@ def run_batch(args, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+SIDE_KEEP = ("value", "unit", "p50_ttft_ms", "ms_per_step", "steps", "warmup", "e2e",
+             "roofline", "sparse_h2d", "full_recompute_ttft_ms", "ttft_speedup_vs_full",
+             "flop_ratio_bound", "gpu_launches", "clocks", "scaling", "n_gpus")
+
+
+def side_configs(args) -> dict:
+    """Configs 3, 4 and 5 measured in the same (default, N = 1) run, each in
+    its own process after the config-2 timed region, so the driver's record
+    carries them: config 3 (64K context, pinned pool), config 4 (ratio sweep +
+    the tuner over real GPU TTFTs, tools/ratio_sweep.py) and config 5 (the
+    64-request batch).  A failure is recorded, it does not fail the line."""
+    me = str(Path(__file__).resolve())
+    jobs = {
+        "cfg3": [me, "--config", "cfg3", "--steps", "3", "--warmup", "3", "--no-cpu",
+                 "--side-configs", "none"],
+        "cfg4": [str(ROOT / "tools" / "ratio_sweep.py"), "--steps", "3"],
+        "cfg5": [me, "--config", "cfg5", "--steps", "2", "--warmup", "3", "--no-cpu",
+                 "--side-configs", "none"],
+    }
+    out = {}
+    for name, cmd in jobs.items():
+        t0 = time.time()
+        try:
+            res = subprocess.run([sys.executable, *cmd], capture_output=True, text=True,
+                                 timeout=args.side_timeout)
+            rows = [ln for ln in res.stdout.splitlines() if ln.startswith("{")]
+            if res.returncode != 0 or not rows:
+                out[name] = {"error": f"exit {res.returncode}: {res.stderr.strip()[-300:]}"}
+                continue
+            d = json.loads(rows[-1])
+            if name != "cfg4":
+                d = {"workload": d.get("config", {}).get("workload"),
+                     **{k: d[k] for k in SIDE_KEEP if k in d}}
+            d["wall_s"] = round(time.time() - t0, 1)
+            out[name] = d
+        except subprocess.TimeoutExpired:
+            out[name] = {"error": f"timed out after {args.side_timeout} s"}
+        print(f"[bench] side config {name}: {time.time() - t0:.0f}s", file=sys.stderr,
+              flush=True)
+    return out
+
+
 def self_launch(n: int) -> int:
     """Re-exec this script under torch.distributed.run with n ranks on this
     node (rendezvous on 127.0.0.1); rank 0 prints the JSON line."""
@@ -893,6 +935,11 @@ def main():
     ap.add_argument("--cpu-rows", type=int, default=32)
     ap.add_argument("--resident-layers", type=int, default=0,
                     help="e2e arm: first n layers of the pinned pool also kept in HBM")
+    ap.add_argument("--side-configs", default="auto", choices=["auto", "none"],
+                    help="auto: a default config-2 run on one GPU also measures configs 3, "
+                         "4 and 5 (separate processes, after the timed region) and embeds "
+                         "them under 'configs'")
+    ap.add_argument("--side-timeout", type=int, default=420)
     ap.add_argument("--dry-run", action="store_true",
                     help="plumbing only: rank/world handling and the max-over-ranks line, "
                          "no GPU work (CPU test of the multi-rank launch)")
@@ -930,7 +977,15 @@ def main():
         if "requests" in CONFIGS[args.config]:
             run_batch(args, rank, world, local_rank)
         else:
-            run_ours(args, rank, world, local_rank)
+            line = run_ours(args, rank, world, local_rank)
+            if line is not None:
+                if (args.side_configs == "auto" and args.config == "cfg2" and world == 1):
+                    import gc
+                    import torch
+                    gc.collect()
+                    torch.cuda.empty_cache()  # the config-2 model and pools are released
+                    line["configs"] = side_configs(args)
+                print(json.dumps(line), flush=True)
     finally:
         if world > 1:
             import torch.distributed as dist

@@ -44,6 +44,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--chunks", type=int, default=16)
+    ap.add_argument("--steps", type=int, default=3, help="timed steps per ratio (p50)")
     args = ap.parse_args()
     cfg = ct.ModelConfig.llama3_8b(n_layers=args.layers, seed=1234)
     model = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
@@ -60,7 +61,7 @@ def main():
         row = {"r": r}
         for name, pool in (("hbm", pool_hbm), ("pinned", pool_pin)):
             eng = SelectivePrefillEngine(model, pool, r, 64)
-            row[f"ttft_ms_{name}"] = p50_ttft(eng)
+            row[f"ttft_ms_{name}"] = p50_ttft(eng, args.steps)
             del eng
             torch.cuda.empty_cache()
         sweep.append(row)
