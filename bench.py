@@ -657,14 +657,14 @@ def run_ours(args, rank, world, local_rank):
                 "ms": scfast, "bytes": scorer_bytes, "bound": "fp32 pipe (ops/B above the ridge)",
                 "hbm_gbs": scorer_bytes / (scfast * 1e-3) / 1e9,
                 "hbm_frac": scorer_bytes / (scfast * 1e-3) / 1e9 / peaks["hbm"],
-                "fp32_pipe_busy_ncu": ncu_field("fs_energy_kernel", "fma_pipe_pct", args.config),
+                "fp32_pipe_busy_ncu": ncu_field("fs_energy_split_kernel", "fma_pipe_pct", args.config),
                 "selection_equals_exact": fast_exact,
                 "chunks_certified_by_guard": int((fast_wcount == 0).sum()),
                 "chunks_rescored": int((fast_wcount > 0).sum()),
                 "chunks_exact_fallback": int((fast_wcount < 0).sum()),
                 "note": "single-precision four-step FFT scores + certified top-k boundary "
                         "(window tokens re-scored in float64); orders exact at k",
-                "traffic": ncu_traffic("fs_energy_kernel", args.config)},
+                "traffic": ncu_traffic("fs_energy_split_kernel", args.config)},
         },
         "offline": offline,
         "step_tflops": step_flops / (p50 * 1e-3) / 1e12,

@@ -5,7 +5,8 @@
 // a selection step that proves the top-k set of the aggregate score equals
 // the float64 one (ct/spectral.py:162-184):
 //
-//   1. fs_energy_kernel: two lanes packed per complex signal (the mask is
+//   1. fs_energy_split_kernel (default band, bf16; below) / fs_energy_kernel
+//      (other bands, f32 or unaligned rows): two lanes packed per complex signal (the mask is
 //      Hermitian, so lowpass(a + ib) = lowpass(a) + i lowpass(b)); the 2048
 //      tokens are n = n2 + 64 n1.  Step 1: 32-point DFT over n1 in registers
 //      (radix-4/2 DIF, compile-time twiddles) and the W_2048^(n2 k1) twiddle;
@@ -398,6 +399,186 @@ fs_energy_kernel(const IN* __restrict__ keys, const IN* __restrict__ values, int
   for (int i = 0; i < 8; ++i) out[q + 32 * (s >> 2) + 64 * (8 * (s & 3) + i)] = acc[i];
 }
 
+// ---------------------------------------------------------------------------
+// Default band (low, cutoff N/4), bf16 rows, 16-byte aligned: the same
+// four-step transform with 512 threads (16 warps, <= 128 registers) instead
+// of 256 at 255 registers -- twice the warps per SM to hide the FMA / shared
+// memory latencies of the register-resident FFT.  Step 1 and step 3 do one
+// 32-point column per thread.  Step 2's 64-point row (k1) is split over a
+// lane pair h = 0, 1 (lanes t, t ^ 8): lane h transforms the samples
+// u[2m + h] (radix-2 decimation in time), so
+//   X[k] = D0[k] + W64^k D1[k],   X[k + 32] = D0[k] - W64^k D1[k].
+// The band keeps k2 < 16 (lane 0) and k2 > 48 (lane 1); everything between
+// is cut, so each lane completes only its 16 surviving bins after one
+// 16-value shuffle exchange, and the inverse split (D0' = X[k] + X[k+32],
+// D1' = W64^-k (X[k] - X[k+32])) needs one more.  Lane 1 works on
+// frequency-shifted copies so both lanes run identical code: its input is
+// multiplied by (-1)^m (its DFT comes out shifted by 16), it holds
+// Z = W64^-(k+48) X[k+48], and its inverse output carries a (-1)^m sign --
+// a sign common to all rows of a column n2, hence to all tokens that step 3
+// builds from it, so every |y|^2 is unchanged.  Per-lane twiddles come
+// from two 2 x 16 shared tables.
+// ---------------------------------------------------------------------------
+__host__ __device__ constexpr int posof32(int f) {
+  int p = 0;
+  for (int i = 0; i < 32; ++i)
+    if (digrev<32>(i) == f) p = i;
+  return p;
+}
+__device__ __forceinline__ cf shfl_xor_cf(cf a, int m) {
+  return make_float2(__shfl_xor_sync(0xffffffffu, a.x, m), __shfl_xor_sync(0xffffffffu, a.y, m));
+}
+// SIG signal slots per batch, 64 SIG threads: SIG = 8 -> one 512-thread CTA
+// per SM (the product), SIG = 4 -> two 256-thread CTAs per SM (measured slower)
+template <int SIG>
+struct Split {
+  static constexpr int THREADS = 64 * SIG;
+  static constexpr int BATCHES = SIG_PER_CTA / SIG;
+  static constexpr int LOG = SIG == 8 ? 3 : 2;
+  static constexpr size_t STAGE = (size_t)N * SIG * 4;
+  // smem: xb [SIG][32][64] cf | T [N] cf | twA [2][16] | twB [2][16] | stage
+  static constexpr size_t SMEM = (size_t)SIG * 32 * 64 * sizeof(cf) + N * sizeof(cf) +
+                                 64 * sizeof(cf) + STAGE;
+  // exchange index: every 16-lane access pattern (steps 1/3: SIG slots x
+  // 16/SIG consecutive n2; step 2: SIG slots x h x two k1) hits 16 distinct
+  // 8-byte slots
+  static __device__ __forceinline__ int xi(int s, int k1, int n2) {
+    const int swz = SIG == 8 ? ((s << 1) ^ (k1 & 1)) : ((s << 2) ^ ((k1 & 1) << 1));
+    return ((s * 32 + k1) << 6) + (n2 ^ swz);
+  }
+};
+
+template <int SIG>
+__global__ void __launch_bounds__(64 * SIG, 8 / SIG)
+fs_energy_split_kernel(const __nv_bfloat16* __restrict__ keys,
+                       const __nv_bfloat16* __restrict__ values, int L, int64_t ld_token,
+                       int64_t ld_layer, int64_t ld_chunk, const float2* __restrict__ tw,
+                       int groups, float* __restrict__ partial) {
+  using S = Split<SIG>;
+  constexpr int TH = S::THREADS;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cf* xb = reinterpret_cast<cf*>(smem_raw);                  // [SIG][32][64]
+  cf* T = xb + SIG * 32 * 64;                                 // W_2048^m
+  cf* twA = T + N;                                            // [h][kk]
+  cf* twB = twA + 32;
+  uint32_t* stg = reinterpret_cast<uint32_t*>(twB + 32);      // [N][SIG] bf16x2
+  const int t = threadIdx.x, s = t & (SIG - 1), q = t >> S::LOG;  // q < 64
+  const int tensor = blockIdx.y, group = blockIdx.x;
+  const int c = blockIdx.z / L, l = blockIdx.z % L;
+  for (int i = t; i < N; i += TH) T[i] = tw[i];
+  if (t < 16) {
+    // forward combine: lane 0 W64^kk, lane 1 W64^-(kk+48); inverse send:
+    // lane 0 W64^-kk, lane 1 W64^(kk+48)  (W64^m = W2048^(32 m))
+    twA[t] = tw[32 * t];
+    twA[16 + t] = tw[512 - 32 * t];
+    twB[t] = tw[(2048 - 32 * t) & (N - 1)];
+    twB[16 + t] = tw[(32 * t + 1536) & (N - 1)];
+  }
+  const __nv_bfloat16* base = (tensor ? values : keys) + (int64_t)c * ld_chunk +
+                              (int64_t)l * ld_layer + (int64_t)group * SIG_PER_CTA * 2;
+  constexpr int NACC = 32 / SIG;
+  float acc[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) acc[i] = 0.f;
+  // batch b's 2 SIG lanes of every token (SIG * 4 bytes): SIG / 4 threads
+  // per token row, 16 bytes each, 256 rows per pass
+  constexpr int PIECES = SIG / 4;
+  auto prefetch = [&](int b) {
+    const int piece = t % PIECES, row = t / PIECES;
+    const __nv_bfloat16* src = base + b * SIG * 2 + piece * 8 + (int64_t)row * ld_token;
+    uint32_t* dst = stg + row * SIG + piece * 4;
+    const int64_t step = (int64_t)(TH / PIECES) * ld_token;
+#pragma unroll 1
+    for (int i = 0; i < N / (TH / PIECES); ++i) {
+      cp_async16(dst, src);
+      src += step;
+      dst += (TH / PIECES) * SIG;
+    }
+    cp_async_commit();
+  };
+  prefetch(0);
+  // step-2 role: row k1 = q >> 1, half h = q & 1 (partner lane t ^ SIG)
+  const int h = q & 1, k1r = q >> 1;
+  const float sg = h ? -1.f : 1.f;
+  const bool cut0 = h && k1r == 0;  // k = 3N/4 (k1 = 0, k2 = 48) is cut
+  __syncthreads();
+
+#pragma unroll 1
+  for (int b = 0; b < S::BATCHES; ++b) {
+    cp_async_wait_all();
+    __syncthreads();
+    // ---- step 1: 32-point DFT over n1 of tokens q + 64 n1, twiddle, exchange
+    {
+      const int n2 = q;
+      cf v[32];
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) v[n1] = unpack_bf16x2(stg[(n2 + 64 * n1) * SIG + s]);
+      fwd<32>(v);
+#pragma unroll
+      for (int p = 0; p < 32; ++p) {
+        const int k1 = digrev<32>(p);
+        xb[S::xi(s, k1, n2)] = cmul(v[p], T[(n2 * k1) & (N - 1)]);
+      }
+    }
+    __syncthreads();
+    if (b + 1 < S::BATCHES) prefetch(b + 1);
+    // ---- step 2: half of row k1r per lane: 32-point DFT of u[2m + h], band
+    // combine over the lane pair, inverse split, 32-point inverse, twiddle
+    {
+      cf v[32];
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        v[m] = xb[S::xi(s, k1r, 2 * m + h)];
+        if (m & 1) v[m] = __fmul2_rn(v[m], make_float2(sg, sg));
+      }
+      fwd<32>(v);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {
+        const cf r = shfl_xor_cf(v[posof32(16 + kk)], SIG);
+        v[posof32(kk)] = v[posof32(kk)] + cmul(r, twA[16 * h + kk]);
+      }
+      if (cut0) v[posof32(0)] = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk)
+        v[posof32(16 + kk)] = shfl_xor_cf(cmul(v[posof32(kk)], twB[16 * h + kk]), SIG);
+      inv<32>(v);
+#pragma unroll
+      for (int m = 0; m < 32; ++m) {
+        const int n2 = 2 * m + h;
+        xb[S::xi(s, k1r, n2)] = cmulc(v[m], T[(n2 * k1r) & (N - 1)]);
+      }
+    }
+    __syncthreads();
+    // ---- step 3: 32-point inverse over k1 -> tokens q + 64 n1', energies
+    float e[32];
+    {
+      const int n2 = q;
+      cf w[32];
+#pragma unroll
+      for (int p = 0; p < 32; ++p) w[p] = xb[S::xi(s, digrev<32>(p), n2)];
+      inv<32>(w);
+#pragma unroll
+      for (int n1 = 0; n1 < 32; ++n1) e[n1] = fmaf(w[n1].x, w[n1].x, w[n1].y * w[n1].y);
+    }
+    // reduce-scatter over the SIG slots (xor SIG/2 ... 1): lane s ends with
+    // n1 in [NACC s, NACC s + NACC)
+#pragma unroll
+    for (int lv = SIG / 2, len = 16; lv >= 1; lv >>= 1, len >>= 1) {
+      const bool up = s & lv;
+#pragma unroll
+      for (int i = 0; i < len; ++i) {
+        const float send = up ? e[i] : e[len + i];
+        e[i] = (up ? e[len + i] : e[i]) + __shfl_xor_sync(0xffffffffu, send, lv);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) acc[i] += e[i];
+  }
+  float* out = partial + ((((int64_t)c * L + l) * 2 + tensor) * groups + group) * N;
+#pragma unroll
+  for (int i = 0; i < NACC; ++i) out[q + 64 * (NACC * s + i)] = acc[i];
+}
+
 __global__ void fs_twiddle(float2* tw) {
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= N) return;
@@ -669,7 +850,16 @@ extern "C" int ct_score_select_fast(const void* keys, const void* values, int dt
   const bool aligned16 = !(((uintptr_t)keys | (uintptr_t)values) & 15) && ld_token % 8 == 0 &&
                          ld_layer % 8 == 0 && ld_chunk % 8 == 0;
   const bool lb = band == 0 && cutoff == fs::N / 4;
-  if (dtype == CT_BF16 && aligned16) {
+  if (dtype == CT_BF16 && aligned16 && lb) {
+    // one 512-thread CTA per SM (SIG = 8); two 256-thread CTAs per SM
+    // (SIG = 4) measured 3 % slower (profiles/round2_scorer_split_ncu.md)
+    auto kern = fs::fs_energy_split_kernel<8>;
+    CT_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)fs::Split<8>::SMEM));
+    kern<<<grid, fs::Split<8>::THREADS, fs::Split<8>::SMEM, st>>>(
+        (const __nv_bfloat16*)keys, (const __nv_bfloat16*)values, (int)L, ld_token, ld_layer,
+        ld_chunk, tw, groups, partial);
+  } else if (dtype == CT_BF16 && aligned16) {
     auto kern = lb ? fs::fs_energy_kernel<__nv_bfloat16, true, true>
                    : fs::fs_energy_kernel<__nv_bfloat16, true, false>;
     const size_t smem_st = smem + fs::STAGE_BYTES;
