@@ -1,0 +1,11 @@
+# attention A/B: previous library vs the current one (split rows off / on)
+set -x
+CT_TC_SPLIT=2 timeout 600 python -m pytest -q -x tests/test_gpu_attention_tc.py 2>&1 | tail -3
+CT_TC_SPLIT=2 timeout 300 python tools/attn_fuzz.py 2>&1 | tail -3
+for rep in 1 2 3; do
+timeout 120 python tools/attn_bench.py --lib tools/probes/bin/lib_base.so --iters 50 | sed 's/^/base   /'
+timeout 120 python tools/attn_bench.py --iters 50 | sed 's/^/split1 /'
+CT_TC_SPLIT=2 timeout 120 python tools/attn_bench.py --iters 50 | sed 's/^/split2 /'
+done
+timeout 120 python tools/attn_bench.py --full | sed 's/^/split1 /'
+CT_TC_SPLIT=2 timeout 120 python tools/attn_bench.py --full | sed 's/^/split2 /'
