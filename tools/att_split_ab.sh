@@ -1,4 +1,5 @@
-# attention A/B: previous library vs the current one (split rows off / on)
+# attention A/B of the round-2 split-row variant (CT_TC_SPLIT=2; the kernel
+# template was not committed; see profiles/round2_attention_probes.md): previous vs current library
 set -x
 CT_TC_SPLIT=2 timeout 600 python -m pytest -q -x tests/test_gpu_attention_tc.py 2>&1 | tail -3
 CT_TC_SPLIT=2 timeout 300 python tools/attn_fuzz.py 2>&1 | tail -3
