@@ -966,6 +966,9 @@ def main():
         # CT_BENCH_DIST=gloo + ranks folded onto the visible GPUs: a functional
         # check of the multi-rank path on a one-GPU box (its timings mean nothing)
         backend = os.environ.get("CT_BENCH_DIST", "nccl")
+        # communicator sizes in the log (the driver's nranks check), also when
+        # the driver launches the ranks with torchrun itself
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
         if backend != "nccl":
             local_rank %= torch.cuda.device_count()
         torch.cuda.set_device(local_rank)
