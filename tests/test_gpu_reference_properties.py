@@ -4,7 +4,8 @@ implementation's drop-in API.
 Sources:
 - scoring and selection: pkg/tests/test_spectral.py;
 - rotary embedding: pkg/tests/test_rope.py;
-- toy-model prefill: pkg/tests/test_toymodel.py:24-140.
+- toy-model prefill: pkg/tests/test_toymodel.py:24-140;
+- chunk pool: pkg/tests/test_cachepool.py:127-210.
 
 The checks are restated, not copied.  They use the same properties and
 tolerances, and run through the GPU scorer (FFT energy kernel, device
@@ -325,3 +326,68 @@ def test_selective_prefill_rejects_a_foreign_ranking(toy):
     other = ct.encode_chunk_isolated(toy, toks(toy, 12, seed=2))
     with pytest.raises(InvalidPlan):
         ct.selective_prefill(toy, [piece], [ct.rank_chunk(other)], [], 0.5)
+
+
+# ------------------------------------------------- chunk pool (CachePool)
+# pkg/tests/test_cachepool.py:127-210, restated: plans and sparse fetches of
+# the registry, with the fetched rows landing in HBM
+
+@pytest.fixture
+def pool16(rng):
+    from paper_2605_24022_b200.pipesim import TierConfig
+    c = chunk_of(rng, 16, layers=3, chunk_id="c0")
+    rk = ct.rank_chunk(c, 0.5)
+    p = ct.CachePool()
+    p.put_chunk(c, rk, TierConfig("cpu-mem", read_bw=20e9, write_bw=20e9))
+    return p, c, rk
+
+
+def test_pool_plans_at_the_ratio_extremes(pool16):
+    from paper_2605_24022_b200.cachepool import token_row_bytes
+    p, c, _ = pool16
+    keep_all = p.plan_sparse_fetch("c0", 0, 0.0)
+    assert len(keep_all.keep_indices) == 16
+    assert keep_all.expected_bytes == 16 * token_row_bytes(2, 4) * 2
+    none = p.plan_sparse_fetch("c0", 1, 1.0)
+    assert len(none.keep_indices) == 0 and none.expected_bytes == 0
+    k, v, keep = p.fetch_sparse(none)
+    assert k is None and v is None and keep.size == 0
+    k, v, keep = p.fetch_sparse(p.plan_sparse_fetch("c0", 2, 0.0))
+    assert np.array_equal(keep, np.arange(16))
+    assert np.array_equal(k.cpu().numpy(), c.keys_raw[2].data)
+    assert np.array_equal(v.cpu().numpy(), c.values[2].data)
+
+
+def test_pool_paper_ratio_and_monotone_bytes(rng, pool16):
+    from paper_2605_24022_b200.pipesim import TierConfig
+    p, _, _ = pool16
+    sizes = [p.plan_sparse_fetch("c0", 0, r).expected_bytes for r in np.linspace(0, 1, 11)]
+    assert all(a >= b for a, b in zip(sizes, sizes[1:]))
+    q = ct.CachePool()
+    c20 = chunk_of(rng, 20, layers=2, chunk_id="p")
+    q.put_chunk(c20, ct.rank_chunk(c20, 0.5), TierConfig("cpu-mem", read_bw=20e9, write_bw=20e9))
+    plan = q.plan_sparse_fetch("p", 0, 0.15)     # 20 tokens, r = 0.15: 17 kept
+    assert len(plan.keep_indices) == 17 and plan.expected_bytes == 17 * 2 * 4 * 4 * 2
+
+
+def test_pool_fetch_plus_recompute_rows_rebuild_the_layer(pool16):
+    p, c, rk = pool16
+    k, _, keep = p.fetch_sparse(p.plan_sparse_fetch("c0", 1, 0.3))
+    rec = ct.indices_for_ratio(rk, 0.3)
+    layer = c.keys_raw[1].data
+    out = ct.tensor_scatter_tokens(ct.SeqTensor(np.zeros_like(layer)),
+                                   ct.SeqTensor(k.cpu().numpy()), keep)
+    out = ct.tensor_scatter_tokens(out, ct.SeqTensor(layer[rec]), rec)
+    assert np.array_equal(np.asarray(out.data), layer)
+
+
+def test_pool_byte_ranges_disjoint_and_coalesced(pool16):
+    from paper_2605_24022_b200.cachepool import token_row_bytes
+    p, _, _ = pool16
+    plan = p.plan_sparse_fetch("c0", 0, 0.2)
+    spans = sorted(plan.byte_ranges)
+    assert sum(n for _, n in spans) == plan.expected_bytes
+    row = token_row_bytes(2, 4)
+    for (o1, n1), (o2, _) in zip(spans, spans[1:]):
+        assert o1 + n1 <= o2                          # disjoint
+        assert o2 != o1 + n1 or n1 % row != 0          # adjacent rows merged
