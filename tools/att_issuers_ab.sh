@@ -1,3 +1,6 @@
+# HISTORICAL: the variant this script selects was measured and removed from the
+# product library (its knob is ignored now); results and source pointers are in
+# profiles/round2_attention_probes.md
 # attention A/B: one MMA issuer for both tiles (default) vs one per tile
 # (CT_TC_ISSUERS=2), tests + fuzzer on the new variant, SM-clock timelines
 set -x

@@ -1,3 +1,6 @@
+# HISTORICAL: the variant this script selects was measured and removed from the
+# product library (its knob is ignored now); results and source pointers are in
+# profiles/round2_attention_probes.md
 # attention A/B: P in TMEM (attention_pp_kernel, default) vs P in shared
 # memory with S(j+1) issued once S(j) is loaded (attention_ps_kernel,
 # CT_TC_PS=1), with FMA-pipe exp2 for 0 / 25 / 50 % of the keys (CT_TC_POLY)

@@ -1,3 +1,6 @@
+# HISTORICAL: the variant this script selects was measured and removed from the
+# product library (its knob is ignored now); results and source pointers are in
+# profiles/round2_attention_probes.md
 # attention A/B: default (P in TMEM, chained) vs P in shared memory with
 # split rows (CT_TC_PSS=1: chain-free, two softmax warps per tile per SMSP)
 set -x
