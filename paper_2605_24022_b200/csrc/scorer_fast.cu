@@ -653,21 +653,25 @@ __global__ void fs_kernel_row(int cutoff, int high, double* p) {
 
 // Exact (float64) energy of the window tokens of one (chunk, layer, tensor):
 // y_w[lane] = sum_n p[(i_w - n) mod N] x[n][lane], E_w = sum_lanes y_w^2.
-// grid: x = chunk (chunks without a re-score window exit), y = tensor,
-// z = layer; 128 threads x 8 lanes (one 16-byte bf16 row piece per tap), R
-// window tokens per pass: one pass over the rows serves R tokens, and the
-// warp-uniform p values are shared-memory broadcasts.
-constexpr int RS_THREADS = 512, RS_LPT = 2, RS_UNROLL = 8;
+// grid: x = chunk (chunks without a re-score window exit), y = 2 layer +
+// tensor, z = group of RS_LANES lanes (so a windowed chunk spreads over
+// 2 L (lanes / RS_LANES) small CTAs); R in {2, 4, 6, 8} window tokens per pass
+// (one pass over the rows serves R tokens); the warp-uniform p values are
+// shared-memory broadcasts.  Each CTA writes its partial energies to its own
+// slot; fs_fixup sums the groups in a fixed order (deterministic).
+constexpr int RS_THREADS = 64, RS_LPT = 4, RS_UNROLL = 8;
+constexpr int RS_LANES = RS_THREADS * RS_LPT;
 template <typename IN>
-__device__ __forceinline__ float2 load2(const IN* p);
+__device__ __forceinline__ float4 load4(const IN* p);
 template <>
-__device__ __forceinline__ float2 load2<__nv_bfloat16>(const __nv_bfloat16* p) {
-  const uint32_t u = __ldg(reinterpret_cast<const unsigned int*>(p));
-  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+__device__ __forceinline__ float4 load4<__nv_bfloat16>(const __nv_bfloat16* p) {
+  const uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+  return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xffff0000u),
+                     __uint_as_float(u.y << 16), __uint_as_float(u.y & 0xffff0000u));
 }
 template <>
-__device__ __forceinline__ float2 load2<float>(const float* p) {
-  return __ldg(reinterpret_cast<const float2*>(p));
+__device__ __forceinline__ float4 load4<float>(const float* p) {
+  return __ldg(reinterpret_cast<const float4*>(p));
 }
 template <int R, typename IN>
 __device__ __forceinline__ void rescore_pass(const IN* __restrict__ x, int lanes, int64_t ld_token,
@@ -676,19 +680,20 @@ __device__ __forceinline__ void rescore_pass(const IN* __restrict__ x, int lanes
   double part[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) part[r] = 0.0;
-  for (int lane0 = threadIdx.x * RS_LPT; lane0 < lanes; lane0 += RS_THREADS * RS_LPT) {
+  for (int lane0 = threadIdx.x * RS_LPT; lane0 < lanes; lane0 += RS_LANES) {
     double y[R][RS_LPT];
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
       for (int i = 0; i < RS_LPT; ++i) y[r][i] = 0.0;
     for (int n0 = 0; n0 < N; n0 += RS_UNROLL) {
-      float2 xv[RS_UNROLL];  // RS_UNROLL rows in flight
+      float4 xv[RS_UNROLL];  // RS_UNROLL rows in flight
 #pragma unroll
-      for (int u = 0; u < RS_UNROLL; ++u) xv[u] = load2<IN>(x + (int64_t)(n0 + u) * ld_token + lane0);
+      for (int u = 0; u < RS_UNROLL; ++u) xv[u] = load4<IN>(x + (int64_t)(n0 + u) * ld_token + lane0);
 #pragma unroll
       for (int u = 0; u < RS_UNROLL; ++u) {
-        const double x4[RS_LPT] = {(double)xv[u].x, (double)xv[u].y};
+        const double x4[RS_LPT] = {(double)xv[u].x, (double)xv[u].y, (double)xv[u].z,
+                                   (double)xv[u].w};
 #pragma unroll
         for (int r = 0; r < R; ++r) {
           const double pv = ps[(tok[r] - n0 - u) & (N - 1)];
@@ -721,38 +726,42 @@ __global__ void __launch_bounds__(RS_THREADS)
 fs_rescore(const IN* __restrict__ keys, const IN* __restrict__ values, int L, int lanes,
            int64_t ld_token, int64_t ld_layer, int64_t ld_chunk, const double* __restrict__ p,
            const int2* __restrict__ win, const int32_t* __restrict__ wcount,
-           const int32_t* __restrict__ order, double* __restrict__ wenergy) {
+           const int32_t* __restrict__ order, double* __restrict__ wpart) {
   const int c = blockIdx.x;
   const int W = wcount[c];
   if (W <= 0 || W > WMAX) return;
   __shared__ double ps[N];
   __shared__ double red[RS_THREADS / 32][8];  // [warp][token]
   __shared__ double res[8];
-  const int tensor = blockIdx.y, l = blockIdx.z;
+  const int l = blockIdx.y >> 1, tensor = blockIdx.y & 1, g = blockIdx.z, groups = gridDim.z;
   const int2 w = win[c];
   for (int i = threadIdx.x; i < N; i += RS_THREADS) ps[i] = p[i];
   __syncthreads();
-  const IN* x = (tensor ? values : keys) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer;
+  const int lane_lo = g * RS_LANES, n_lanes = min(RS_LANES, lanes - lane_lo);
+  const IN* x = (tensor ? values : keys) + (int64_t)c * ld_chunk + (int64_t)l * ld_layer + lane_lo;
   for (int r0 = 0; r0 < W; r0 += 8) {
     const int nr = min(8, W - r0);
     int tok[8];
 #pragma unroll
     for (int r = 0; r < 8; ++r) tok[r] = r < nr ? order[(int64_t)c * N + w.x + r0 + r] : 0;
     if (nr <= 2)
-      rescore_pass<2, IN>(x, lanes, ld_token, ps, tok, nr, red, res);
+      rescore_pass<2, IN>(x, n_lanes, ld_token, ps, tok, nr, red, res);
     else if (nr <= 4)
-      rescore_pass<4, IN>(x, lanes, ld_token, ps, tok, nr, red, res);
+      rescore_pass<4, IN>(x, n_lanes, ld_token, ps, tok, nr, red, res);
+    else if (nr <= 6)
+      rescore_pass<6, IN>(x, n_lanes, ld_token, ps, tok, nr, red, res);
     else
-      rescore_pass<8, IN>(x, lanes, ld_token, ps, tok, nr, red, res);
+      rescore_pass<8, IN>(x, n_lanes, ld_token, ps, tok, nr, red, res);
     if ((int)threadIdx.x < nr)
-      wenergy[(((int64_t)c * WMAX + r0 + threadIdx.x) * L + l) * 2 + tensor] = res[threadIdx.x];
+      wpart[((((int64_t)c * WMAX + r0 + threadIdx.x) * L + l) * 2 + tensor) * groups + g] =
+          res[threadIdx.x];
   }
 }
 
 // Exact window scores -> window re-ordered by (score desc, index asc).
 __global__ void fs_fixup(int C, const int2* __restrict__ win, const int32_t* __restrict__ wcount,
-                         const double* __restrict__ wenergy, int L, int32_t* __restrict__ order,
-                         double* __restrict__ agg) {
+                         const double* __restrict__ wpart, int groups, int L,
+                         int32_t* __restrict__ order, double* __restrict__ agg) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C || wcount[c] <= 0 || wcount[c] > WMAX) return;
   const int slot = c;
@@ -764,7 +773,13 @@ __global__ void fs_fixup(int C, const int2* __restrict__ win, const int32_t* __r
   for (int r = 0; r < W; ++r) {
     double acc = 0.0;
     for (int l = 0; l < L; ++l) {
-      const double* e = wenergy + (((int64_t)slot * WMAX + r) * L + l) * 2;
+      double e[2];
+      for (int t = 0; t < 2; ++t) {  // lane groups summed in order
+        const double* q = wpart + ((((int64_t)slot * WMAX + r) * L + l) * 2 + t) * groups;
+        double v = 0.0;
+        for (int g = 0; g < groups; ++g) v += q[g];
+        e[t] = v;
+      }
       acc += 0.5 * sqrt(e[0]) + 0.5 * sqrt(e[1]);
     }
     sc[r] = acc / (double)L;
@@ -797,6 +812,7 @@ extern "C" int ct_desc_order(const double* scores, int64_t rows, int64_t n, int3
                              void* stream);
 
 static size_t fs_groups(int64_t lanes) { return (size_t)(lanes / (2 * fs::SIG_PER_CTA)); }
+static size_t fs_rs_groups(int64_t lanes) { return (size_t)((lanes + fs::RS_LANES - 1) / fs::RS_LANES); }
 
 extern "C" size_t ct_score_fast_workspace_bytes(int64_t C, int64_t L, int64_t N, int64_t lanes) {
   if (N != fs::N || lanes % (2 * fs::SIG_PER_CTA)) return 0;
@@ -804,7 +820,7 @@ extern "C" size_t ct_score_fast_workspace_bytes(int64_t C, int64_t L, int64_t N,
   b += align_up((size_t)N * sizeof(float2), 256);                 // twiddles
   b += align_up((size_t)N * sizeof(double), 256);                 // projection row
   b += align_up((size_t)C * sizeof(int2), 256);                   // windows
-  b += align_up((size_t)C * fs::WMAX * L * 2 * sizeof(double), 256);  // window energies
+  b += align_up((size_t)C * fs::WMAX * L * 2 * fs_rs_groups(lanes) * sizeof(double), 256);  // window energies
   return b;
 }
 
@@ -822,6 +838,16 @@ extern "C" int ct_score_select_fast(const void* keys, const void* values, int dt
     return fail(CT_ERR_UNSUPPORTED, "fast scorer needs N = %d and lanes %% %d == 0 (N=%lld)",
                 fs::N, 2 * fs::SIG_PER_CTA, (long long)N);
   if (!valid_dtype(dtype)) return fail(CT_ERR_PARAM, "dtype %d", dtype);
+  {
+    // the window re-score reads 4 lanes per load: 8-byte (bf16) / 16-byte
+    // (f32) aligned rows
+    const int64_t vec = 4;  // elements per load
+    const uintptr_t abytes = dtype == CT_BF16 ? 8 : 16;
+    if ((((uintptr_t)keys | (uintptr_t)values) & (abytes - 1)) || ld_token % vec ||
+        ld_layer % vec || ld_chunk % vec)
+      return fail(CT_ERR_UNSUPPORTED, "fast scorer needs %d-byte aligned rows",
+                  (int)abytes);
+  }
   if (band != 0 && band != 1) return fail(CT_ERR_PARAM, "band %d", band);
   if (cutoff < 0 || cutoff > N / 2 + 1) return fail(CT_ERR_PARAM, "cutoff %lld", (long long)cutoff);
   if (k < 0 || k > N) return fail(CT_ERR_PARAM, "k %lld", (long long)k);
@@ -895,7 +921,9 @@ extern "C" int ct_score_select_fast(const void* keys, const void* values, int dt
   // the call never waits for the window counts on the host
   fs::fs_kernel_row<<<(fs::N + 255) / 256, 256, 0, st>>>((int)cutoff, band, prow);
   if ((rc = check_launch("fs_kernel_row"))) return rc;
-  dim3 rgrid((unsigned)C, 2, (unsigned)L);
+  const int rs_groups = (int)fs_rs_groups(lanes);
+  if (2 * L > 65535) return fail(CT_ERR_UNSUPPORTED, "2 L too large for the re-score grid");
+  dim3 rgrid((unsigned)C, (unsigned)(2 * L), (unsigned)rs_groups);
   if (dtype == CT_BF16)
     fs::fs_rescore<__nv_bfloat16><<<rgrid, fs::RS_THREADS, 0, st>>>(
         (const __nv_bfloat16*)keys, (const __nv_bfloat16*)values, (int)L, (int)lanes, ld_token,
@@ -905,7 +933,7 @@ extern "C" int ct_score_select_fast(const void* keys, const void* values, int dt
                                                  (int)lanes, ld_token, ld_layer, ld_chunk, prow,
                                                  win, wcount, agg_order, wenergy);
   if ((rc = check_launch("fs_rescore"))) return rc;
-  fs::fs_fixup<<<(unsigned)((C + 63) / 64), 64, 0, st>>>((int)C, win, wcount, wenergy, (int)L,
+  fs::fs_fixup<<<(unsigned)((C + 63) / 64), 64, 0, st>>>((int)C, win, wcount, wenergy, rs_groups, (int)L,
                                                          agg_order, agg_scores);
   return check_launch("fs_fixup");
 }
