@@ -71,3 +71,37 @@ def test_reference_arm_reports_host_info():
     d = json.loads([l for l in _run().stdout.splitlines() if l.startswith("{")][0])
     host = d["cpu_baseline"]["host"]
     assert host["cpu_count"] >= 1 and host["numpy"] and "threads_env" in host
+
+
+def test_side_configs_record_failures(monkeypatch):
+    """bench.side_configs embeds configs 3-5 from child processes; a child
+    that fails, prints nothing or times out is recorded under its name instead
+    of failing the config-2 line."""
+    import importlib.util
+    import subprocess as sp
+    spec = importlib.util.spec_from_file_location("bench_mod", ROOT / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+
+    calls = []
+
+    def fake_run(cmd, capture_output, text, timeout):
+        calls.append(cmd)
+        name = cmd[cmd.index("--config") + 1] if "--config" in cmd else "cfg4"
+        if name == "cfg3":
+            return sp.CompletedProcess(cmd, 0, stdout='{"value": 4.0, "config": {"workload": "w3"}, '
+                                                      '"p50_ttft_ms": 250.0, "extra": 1}\n', stderr="")
+        if name == "cfg4":
+            return sp.CompletedProcess(cmd, 1, stdout="", stderr="boom")
+        raise sp.TimeoutExpired(cmd, timeout)
+
+    monkeypatch.setattr(bench.subprocess, "run", fake_run)
+
+    class A:
+        side_timeout = 5
+    out = bench.side_configs(A())
+    assert len(calls) == 3
+    assert out["cfg3"]["value"] == 4.0 and out["cfg3"]["workload"] == "w3"
+    assert "extra" not in out["cfg3"] and out["cfg3"]["wall_s"] >= 0
+    assert out["cfg4"]["error"].startswith("exit 1") and "boom" in out["cfg4"]["error"]
+    assert "timed out" in out["cfg5"]["error"]
