@@ -43,6 +43,9 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--out", default="")
     ap.add_argument("--torch-bf16", action="store_true")
+    ap.add_argument("--config", default="cfg2", choices=["cfg2", "cfg3"],
+                    help="cfg3: Mistral-7B geometry, 32 x 2048 + 64 = 65,600 tokens, pool in "
+                         "pinned host memory (the sparse-H2D path)")
     args = ap.parse_args()
     import torch
     import paper_2605_24022_b200 as ct
@@ -50,8 +53,13 @@ def main():
     from paper_2605_24022_b200.pipeline import SelectivePrefillEngine
     from paper_2605_24022_b200.pool import KvPool
 
-    C, N, S, R = 16, 2048, 64, 0.15
-    cfg = ct.ModelConfig.llama3_8b(n_layers=args.layers, seed=args.seed + 21)
+    N, S, R = 2048, 64, 0.15
+    if args.config == "cfg3":
+        C, where = 32, "pinned"
+        cfg = ct.ModelConfig.mistral_7b(n_layers=args.layers, seed=args.seed + 21)
+    else:
+        C, where = 16, "hbm"
+        cfg = ct.ModelConfig.llama3_8b(n_layers=args.layers, seed=args.seed + 21)
     model = ct.GpuModel.random(cfg, dtype=torch.bfloat16)
     rng = np.random.default_rng(args.seed)
     toks = [rng.integers(0, cfg.vocab_size, size=N) for _ in range(C)]
@@ -59,7 +67,7 @@ def main():
     t0 = time.time()
     chunks = [ct.encode_chunk_isolated(model, t, chunk_id=f"c{j}") for j, t in enumerate(toks)]
     ranks = ct.rank_chunks(chunks)
-    eng = SelectivePrefillEngine(model, KvPool(chunks, ranks, "hbm"), R, S)
+    eng = SelectivePrefillEngine(model, KvPool(chunks, ranks, where), R, S)
     logits = eng.step(torch.as_tensor(suffix.astype(np.int32), device="cuda"))
     torch.cuda.synchronize()
     got = logits.double().cpu().numpy().reshape(-1)
@@ -83,8 +91,9 @@ def main():
     want = np.asarray(res["logits"]).reshape(-1)
     want_k, want_v = res["kv"][-1]
     cpu_s = time.time() - t1
-    out = {"workload": f"config-2 context (16 x 2048 + 64 = 32832 tokens), Llama-3-8B layer "
-                       f"geometry, {args.layers} layers, r = 0.15, bf16 mode",
+    geo = "Mistral-7B" if args.config == "cfg3" else "Llama-3-8B"
+    out = {"workload": f"{args.config} context ({C} x {N} + {S} = {C * N + S} tokens), {geo} "
+                       f"layer geometry, {args.layers} layers, r = 0.15, bf16 mode, pool in {where}",
            "logits_normwise_rel": O.normwise_rel(got, want),
            "last_layer_k_normwise_rel": O.normwise_rel(got_k, want_k),
            "last_layer_v_normwise_rel": O.normwise_rel(got_v, want_v),
