@@ -636,7 +636,14 @@ def run_ours(args, rank, world, local_rank):
                      "frac": att_tflops / peaks["bf16_sust"],
                      "traffic": ncu_traffic("attention_pp_kernel", args.config),
                      "flops_per_launch": att_flops, "launch_ms": att_ms,
-                     "peak_source": peaks["src"] + " bf16 sustained"},
+                     "peak_source": peaks["src"] + " bf16 sustained",
+                     # per-clock utilisation from the committed ncu capture:
+                     # at D = 128 the tensor and MUFU work per key block are
+                     # equal (profiles/round2_attention_probes.md)
+                     "tensor_pipe_active_ncu": ncu_field("attention_pp_kernel",
+                                                         "tensor_pipe_pct", args.config),
+                     "mufu_pipe_active_ncu": ncu_field("attention_pp_kernel",
+                                                       "mufu_pipe_pct", args.config)},
         "kernels": {
             "gather_rope_blend": {"bound": "hbm", "achieved": blend_gbs, "peak": peaks["hbm"],
                                   "unit": "GB/s", "frac": blend_gbs / peaks["hbm"],
