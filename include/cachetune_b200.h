@@ -281,6 +281,14 @@ int ct_residual_rmsnorm(float* h, const void* delta, int delta_dtype, int64_t A,
 int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype,
                int kind, void* act, int act_dtype, void* stream);
 
+/* act[m][i] = silu(g) * u with g = (x @ w)[m][i], u = (x @ w)[m][I + i]: the
+ * SwiGLU gate/up projection and activation of ct/toymodel.py:184-186 in one
+ * tcgen05 kernel (bf16 x [M][K] row stride ldx, w [K][2I] row stride ldw,
+ * act [M][I] row stride ld_act; f32 accumulation, the [M][2I] product never
+ * stored).  K % 64 == 0, I % 128 == 0, 16-byte aligned rows. */
+int ct_gemm_swiglu(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
+                   int64_t I, int64_t ldw, void* act, int64_t ld_act, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* (2) sparse pinned-host -> HBM transfer on the copy engines
  * (ct/cachepool.py:409-481 with an importance-ordered pool so each

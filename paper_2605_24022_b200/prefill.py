@@ -124,6 +124,26 @@ def _record_mode(record):
     return False, int(record)
 
 
+# CT_MLP_FUSED=0 (read once) keeps the bf16 SwiGLU MLP on cuBLAS + ct_mlp_act
+# (the A/B baseline of the fused tcgen05 gate/up kernel)
+_MLP_FUSED_ENV = __import__("os").environ.get("CT_MLP_FUSED", "1") != "0"
+# row range of the fused kernel, from end-to-end A/B (CT_MLP_FUSED=0/1):
+# below 128 rows a tile is mostly padding; at config 2's 4,992 active rows it
+# saves 2.8 ms per request (96.1 -> 93.3 ms); at 9,920 rows (config 3) it is
+# neutral to 0.5 % slower and at 32K rows (full prefill) 3.5 % slower than
+# cuBLAS's two-CTA 256 x 256 tiles + the separate SwiGLU kernel, so larger
+# calls keep that path and each path runs its faster implementation
+FUSED_MIN_ROWS, FUSED_MAX_ROWS = 128, 8192
+
+
+def _fused_mlp(model: GpuModel) -> bool:
+    """bf16 SwiGLU with tile-friendly widths: gate/up + activation in one
+    tcgen05 kernel (ct_gemm_swiglu)."""
+    cfg = model.config
+    return (_MLP_FUSED_ENV and model.dtype == torch.bfloat16 and cfg.mlp_kind == "swiglu"
+            and cfg.hidden_dim % 64 == 0 and cfg.inter % 128 == 0)
+
+
 class LayerBuffers:
     """Per-run activations (reused across layers)."""
 
@@ -138,7 +158,11 @@ class LayerBuffers:
         self.q = torch.empty((a, cfg.n_heads, d), dtype=dt, device=dev)
         self.ctx = torch.empty((a, cfg.n_heads * d), dtype=dt, device=dev)
         width = {"relu": 4 * hid, "swiglu": 2 * cfg.inter}.get(cfg.mlp_kind, 0)
-        self.gu = torch.empty((a, width), dtype=dt, device=dev) if width else None
+        # the bf16 SwiGLU MLP runs fused (ct_gemm_swiglu) for >= FUSED_MIN_ROWS
+        # rows, so its [rows, 2I] gate/up buffer only serves smaller calls
+        gu_rows = (min(a, FUSED_MIN_ROWS) if cfg.mlp_kind == "swiglu" and _fused_mlp(model)
+                   and a <= FUSED_MAX_ROWS else a)
+        self.gu = torch.empty((gu_rows, width), dtype=dt, device=dev) if width else None
         self.act = torch.empty((a, width // 2 if cfg.mlp_kind == "swiglu" else width),
                                dtype=dt, device=dev) if width else None
 
@@ -271,11 +295,17 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
         if kind:
             up = w["w1"] if kind == "relu" else w["wgu"]
             down = w["w2"] if kind == "relu" else w["wd"]
-            guv, actv = buf.gu[r0:], buf.act[r0:]
-            torch.mm(xv, up, out=guv)
+            actv = buf.act[r0:]
             inter = buf.act.shape[1]
-            _lib.call("ct_mlp_act", _dev.ptr(guv), av, inter, dtc, 1 if kind == "relu" else 0,
-                      _dev.ptr(actv), dtc, st)
+            if (kind == "swiglu" and FUSED_MIN_ROWS <= av <= FUSED_MAX_ROWS
+                    and _fused_mlp(model)):
+                _lib.call("ct_gemm_swiglu", _dev.ptr(xv), av, hid, xv.stride(0), _dev.ptr(up),
+                          inter, up.stride(0), _dev.ptr(actv), actv.stride(0), st)
+            else:
+                guv = buf.gu[:av]
+                torch.mm(xv, up, out=guv)
+                _lib.call("ct_mlp_act", _dev.ptr(guv), av, inter, dtc,
+                          1 if kind == "relu" else 0, _dev.ptr(actv), dtc, st)
             _residual_mm(hv, actv, down)
             _lib.call("ct_residual_rmsnorm", _dev.ptr(hv), None, _lib.CT_F32, av,
                       hid, NORM_EPS, _dev.ptr(xv), dtc, st)

@@ -28,6 +28,7 @@ run memcheck memkernels 300 1 tests/test_gpu_memkernels.py
 run memcheck scorer_fast 300 1 tests/test_gpu_scorer_fast.py
 run memcheck attention_tc 300 1 tests/test_gpu_attention_tc.py -k "matches_torch or f32_output or few_row"
 run memcheck pool 300 1 tests/test_gpu_pool.py -k "plans_match or more_chunks or fetch_only or permute"
+run memcheck gemm_swiglu 300 1 tests/test_gpu_gemm_swiglu.py -k "not 4992 and not 9920"
 run initcheck memkernels 300 0 tests/test_gpu_memkernels.py -k "blend"
 run initcheck parity 400 0 tests/test_gpu_parity.py -k "spectral_cases or rope_cases or fuse_cases or config1"
 run initcheck attention_tc 300 0 tests/test_gpu_attention_tc.py -k "f32_output or few_row"
@@ -36,4 +37,6 @@ run synccheck attention_tc 300 1 tests/test_gpu_attention_tc.py -k "f32_output"
 run racecheck scorer 400 1 tests/test_gpu_parity.py -k "spectral_cases and not big"
 run racecheck scorer_fast 400 1 tests/test_gpu_scorer_fast.py -k "rejects or window"
 run racecheck attention_tc 400 1 tests/test_gpu_attention_tc.py -k "f32_output"
+run racecheck gemm_swiglu 300 1 tests/test_gpu_gemm_swiglu.py -k "128-64-128 or 129-512-384"
+run synccheck gemm_swiglu 300 1 tests/test_gpu_gemm_swiglu.py -k "128-64-128 or 129-512-384"
 exit 0
