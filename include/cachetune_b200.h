@@ -289,6 +289,19 @@ int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype,
 int ct_gemm_swiglu(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
                    int64_t I, int64_t ldw, void* act, int64_t ld_act, void* stream);
 
+/* The dense projections of the bf16 step (ct/toymodel.py:176-189) on the
+ * same CTA-pair tcgen05 GEMM: x bf16 [M][K] (row stride ldx) times w bf16
+ * [K][N] (row stride ldw), f32 accumulation, and
+ *   out_dtype CT_BF16, accumulate 0: out bf16 [M][N]  = x @ w   (QKV)
+ *   out_dtype CT_F32,  accumulate 1: out f32  [M][N] += x @ w   (O- and
+ *     down-projection into the f32 residual stream)
+ * K % 64 == 0, N % 128 == 0, 16-byte aligned rows; other combinations
+ * return CT_ERR_UNSUPPORTED.  Tiles are 256 x 256 per CTA pair, or 256 x 128
+ * when that fills the last wave of tiles better. */
+int ct_gemm_bf16(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w, int64_t N,
+                 int64_t ldw, void* out, int64_t ld_out, int out_dtype, int accumulate,
+                 void* stream);
+
 /* ------------------------------------------------------------------ */
 /* (2) sparse pinned-host -> HBM transfer on the copy engines
  * (ct/cachepool.py:409-481 with an importance-ordered pool so each

@@ -5,20 +5,35 @@
 // geometry): the [M, 2I] gate/up product never reaches HBM, and the
 // activation is computed from the f32 accumulators.
 //
-// C tile = 128 rows x 256 accumulator columns = 128 gate + the matching 128
-// up columns, so one N-tile yields 128 finished activation columns.
-//   warp 0   TMA producer: per 64-deep K stage one A box (64 K x 128 rows,
-//            K-major) and four B boxes (64 N x 64 K, MN-major: 2 gate + 2 up),
-//            SWIZZLE_128B, a 4-stage ring (48 KiB per stage)
-//   warp 1   MMA issuer: tcgen05.mma kind::f16 M128 N256 K16, f32 in TMEM
-//            (+ TMEM allocation)
-//   warps 2-5 epilogue: one TMEM lane (= output row) per thread,
-//            silu(g) * u in f32, bf16 16-byte stores
+// Default: a CTA pair (cluster of 2 on one TPC, tcgen05 cta_group::2).  One
+// MMA tile = 256 rows x 256 accumulator columns = 128 gate + the matching 128
+// up columns, so one N-tile yields 128 finished activation columns; CTA r of
+// the pair holds rows [128 r, 128 r + 128) of x and half of B (r = 0 the gate
+// columns, r = 1 the up columns), and its TMEM receives all 256 columns of
+// its own 128 rows.  Per CTA and 64-deep K stage: 16 KiB of A + 16 KiB of B
+// (the 1-SM M128 N256 form reads 48 KiB of operands from shared memory for
+// the same 128 x 256 x 64 MACs per SM).  Config-2 shape (4992 x 4096 x
+// 2 x 14336) under ncu: 743.5 us at 1.435 GHz = 1.58 PFLOP/s, 96 % of the
+// dense bf16 peak at that clock (profiles/round2_gemm_swiglu_ncu.md).
+//   warp 0   TMA producer (both CTAs): A box 64 K x 128 rows (K-major), two
+//            B boxes 64 N x 64 K (MN-major), SWIZZLE_128B; completion bytes
+//            of both CTAs land on the leader's full barrier
+//   warp 1   TMEM allocation (both CTAs); MMA issuer (leader only):
+//            tcgen05.mma.cta_group::2 kind::f16 M256 N256 K16, commits
+//            multicast to the stage / accumulator barriers of both CTAs
+//   warps 2-5 epilogue (both CTAs): one TMEM lane (= output row) per thread,
+//            silu(g) * u in f32, bf16 16-byte stores; each warp releases the
+//            accumulator on the leader's barrier
+// The same kernel serves the step's other projections through ct_gemm_bf16
+// (epilogue STORE: bf16 out = x @ w; ADD: f32 out += x @ w), with tiles of
+// 256 x 256 output columns (128 per CTA of B) or 256 x 128 when N % 256 != 0.
+// NCTA = 1 (CT_GEMM_1SM=1) is the single-SM form (M128 N256, all four B
+// boxes in one CTA), kept for A/B.
 // TMEM holds two 256-column accumulators, so the epilogue of tile t runs
-// under the MMAs of tile t+1.  Persistent: one CTA per SM walks the tiles
-// N-major within L2-sized bands of M-tiles (TileMap), so consecutive CTAs
-// share the B tile and the A slice stays in L2.  Rows past M are zero-filled
-// by TMA and not stored.
+// under the MMAs of tile t+1.  Persistent: one CTA (pair) per SM (TPC) walks
+// the tiles N-major within L2-sized bands of M-tiles (TileMap), so
+// consecutive pairs share the B tile and the A slice stays in L2.  Rows past
+// M are zero-filled by TMA and not stored.
 #include "common.cuh"
 
 #include <cuda.h>
@@ -28,13 +43,17 @@
 namespace ct {
 namespace gm {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64;  // rows per CTA, K per stage
 constexpr int A_BYTES = BM * BK * 2;          // 16 KiB
-constexpr int B_BYTES = BN * BK * 2;          // 32 KiB: four 64 x 64 N-atoms
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int NBAR = 2 * STAGES + 4;
-constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + NBAR * 8 + 16 + 1024;
-
+template <int NCTA, int BNT>  // BNT: accumulator columns per tile (256 or 128)
+struct Cfg {
+  static constexpr int ATOMS = BNT / 64 / NCTA;  // 64 x 64 B atoms held by this CTA
+  static constexpr int B_BYTES = ATOMS * 8192;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES > 8 ? 8 : (192 * 1024) / STAGE_BYTES;
+  static constexpr int NBAR = 2 * STAGES + 4;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + NBAR * 8 + 16 + 1024;
+};
 __device__ __forceinline__ uint32_t su32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -81,6 +100,50 @@ __device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t
       "l"(a), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
+// ---- CTA-pair (cta_group::2) forms
+// TMA into this CTA's shared memory, completion bytes on the leader's barrier
+// (clearing the peer bit of the shared::cluster address selects CTA 0)
+__device__ __forceinline__ void tma2d_pair(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0,
+                                           int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(dst),
+      "l"(m), "r"(bar & 0xFEFFFFFFu), "r"(c0), "r"(c1)
+      : "memory");
+}
+// arrive on the same barrier of both CTAs when the issued MMAs complete
+__device__ __forceinline__ void commit_pair(uint32_t b) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(b),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t d, uint64_t a, uint64_t b, uint32_t id,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc)
+      : "memory");
+}
+// arrive on barrier `b` (a local shared address) of cluster CTA 0
+__device__ __forceinline__ void mbar_arrive_leader(uint32_t b) {
+  asm volatile(
+      "{\n\t.reg .b32 ra;\n\tmapa.shared::cluster.u32 ra, %0, 0;\n\t"
+      "mbarrier.arrive.release.cluster.shared::cluster.b64 _, [ra];\n\t}" ::"r"(b)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
 // shared-memory matrix descriptor, SWIZZLE_128B, sm100 version bit
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
   uint64_t d = 0;
@@ -133,42 +196,71 @@ struct TileMap {
   }
 };
 
+// epilogues: SWIGLU act = silu(g) * u (bf16, B columns = gate | up halves of
+// width I); STORE out = x @ w (bf16); ADD out += x @ w (f32 residual, the
+// beta = 1 GEMM of the O- and down-projections)
+enum Mode { SWIGLU = 0, STORE = 1, ADD = 2 };
+
+template <int NCTA, int MODE, int BNT>
 __global__ void __launch_bounds__(192, 1)
-gemm_swiglu_kernel(const __grid_constant__ CUtensorMap map_x,
-                   const __grid_constant__ CUtensorMap map_w, __nv_bfloat16* __restrict__ act,
-                   int M, int I, int K, int64_t ld_act, int band_m) {
+gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
+            void* __restrict__ out, int M, int N, int K, int64_t ld_out, int band_m) {
+  // N: activation width I (SWIGLU) or output columns
+  static_assert(MODE != SWIGLU || BNT == 256, "SWIGLU tiles pair 128 gate + 128 up columns");
+  using C = Cfg<NCTA, BNT>;
+  constexpr int STAGES = C::STAGES, STAGE_BYTES = C::STAGE_BYTES;
+  constexpr bool PAIR = NCTA == 2;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = su32(smem_raw);
-  const uint32_t base = (raw + 1023u) & ~1023u;
+  const uint32_t base = (raw + 1023u) & ~1023u;  // the same offset in both CTAs of a pair
   uint8_t* gbase = smem_raw + (base - raw);
   const uint32_t bar = base + STAGES * STAGE_BYTES;
   auto full = [&](int s) { return bar + s * 8; };
   auto empty = [&](int s) { return bar + (STAGES + s) * 8; };
   auto afull = [&](int b) { return bar + (2 * STAGES + b) * 8; };
   auto aempty = [&](int b) { return bar + (2 * STAGES + 2 + b) * 8; };
-  uint32_t* tptr = reinterpret_cast<uint32_t*>(gbase + STAGES * STAGE_BYTES + NBAR * 8);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int mt = (M + BM - 1) / BM, nt = I / 128, tiles = mt * nt, kt = K / BK;
+  const int rank = PAIR ? (int)cluster_rank() : 0;
+  // TMEM address slot at the same offset in both CTAs: the pair allocation
+  // writes it for the pair (a per-rank slot leaves rank 1's unwritten), so
+  // racecheck reports the two CTAs' allocations writing the same value here
+  // (profiles/round2_sanitizer.md); both complete before the cluster barrier
+  // that precedes the read
+  uint32_t* tptr = reinterpret_cast<uint32_t*>(gbase + STAGES * STAGE_BYTES + C::NBAR * 8);
+  const int unit = blockIdx.x / NCTA, units = gridDim.x / NCTA;  // pair index / pairs
+  constexpr int TM = BM * NCTA;                                   // rows per MMA tile
+  const int mt = (M + TM - 1) / TM, nt = MODE == SWIGLU ? N / 128 : N / BNT;
+  const int tiles = mt * nt, kt = K / BK;
   const TileMap tm{mt, nt, band_m};
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full(s), 1);
+      mbar_init(full(s), 1);  // the leader's expect_tx (pair: both CTAs' bytes)
       mbar_init(empty(s), 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(afull(b), 1);
-      mbar_init(aempty(b), 128);
+      mbar_init(aempty(b), 4 * NCTA);  // one arrival per epilogue warp of the pair
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-                     su32(tptr))
-                 : "memory");
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tptr)), "n"(2 * BNT)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       su32(tptr)), "n"(2 * BNT)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // barrier inits and the allocation visible to the peer
+  else
+    __syncthreads();
   fence_after();
   const uint32_t tmem = *tptr;
   if (warp == 0) {
@@ -176,19 +268,34 @@ gemm_swiglu_kernel(const __grid_constant__ CUtensorMap map_x,
     if (lane == 0) {
       int s = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+      for (int t = unit; t < tiles; t += units) {
         int m_i, n_i;
         tm.at(t, m_i, n_i);
+        const int row0 = m_i * TM + rank * BM;
         for (int k = 0; k < kt; ++k) {
           mbar_wait(empty(s), ph ^ 1);
           const uint32_t st = base + s * STAGE_BYTES;
-          mbar_expect_tx(full(s), STAGE_BYTES);
-          tma2d(st, &map_x, full(s), k * BK, m_i * BM);
-          // N-atoms: gate [128 n, +64), [+64, +128), up [I + 128 n, ...)
+          if constexpr (PAIR) {
+            if (rank == 0) mbar_expect_tx(full(s), 2 * STAGE_BYTES);
+            tma2d_pair(st, &map_x, full(s), k * BK, row0);
+            // this CTA's half of B: SWIGLU rank 0 gate [128 n, +128), rank 1 up
+            // [N + 128 n, ...); otherwise columns [256 n + 128 rank, +128)
+            const int c0 = MODE == SWIGLU ? rank * N + n_i * 128 : n_i * BNT + rank * (BNT / 2);
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
-            tma2d(st + A_BYTES + i * 8192, &map_w, full(s),
-                  (i < 2 ? 0 : I) + n_i * 128 + (i & 1) * 64, k * BK);
+            for (int i = 0; i < C::ATOMS; ++i)
+              tma2d_pair(st + A_BYTES + i * 8192, &map_w, full(s), c0 + i * 64, k * BK);
+          } else {
+            mbar_expect_tx(full(s), STAGE_BYTES);
+            tma2d(st, &map_x, full(s), k * BK, row0);
+            // N-atoms: SWIGLU gate [128 n, +64), [+64, +128), up [N + 128 n, ...);
+            // otherwise [BNT n + 64 i, +64)
+#pragma unroll
+            for (int i = 0; i < C::ATOMS; ++i)
+              tma2d(st + A_BYTES + i * 8192, &map_w, full(s),
+                    MODE == SWIGLU ? (i < 2 ? 0 : N) + n_i * 128 + (i & 1) * 64
+                                   : n_i * BNT + i * 64,
+                    k * BK);
+          }
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
@@ -198,33 +305,43 @@ gemm_swiglu_kernel(const __grid_constant__ CUtensorMap map_x,
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      // kind::f16, bf16 A/B, f32 D, A K-major, B MN-major, N = 256, M = 128
+    if (lane == 0 && rank == 0) {
+      // kind::f16, bf16 A/B, f32 D, A K-major, B MN-major, N = BNT, M = 128 NCTA
       constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (1u << 16) |
-                                 ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+                                 ((uint32_t)(BNT >> 3) << 17) | ((uint32_t)(TM >> 4) << 24);
       int s = 0, it = 0;
       uint32_t ph = 0;
-      for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      for (int t = unit; t < tiles; t += units, ++it) {
         const int b = it & 1;
         mbar_wait(aempty(b), (uint32_t)(((it >> 1) & 1) ^ 1));
         fence_after();
-        const uint32_t acc = tmem + (uint32_t)(b * 256);
+        const uint32_t acc = tmem + (uint32_t)(b * BNT);
         for (int k = 0; k < kt; ++k) {
           mbar_wait(full(s), ph);
           fence_after();
           const uint32_t st = base + s * STAGE_BYTES;
           const uint64_t ad = sdesc(st, 16, 1024), bd = sdesc(st + A_BYTES, 8192, 1024);
 #pragma unroll
-          for (int kk = 0; kk < BK / 16; ++kk)
-            mma(acc, ad + (uint64_t)((kk * 32) >> 4), bd + (uint64_t)((kk * 2048) >> 4), IDESC,
-                (k | kk) ? 1u : 0u);
-          commit(empty(s));
+          for (int kk = 0; kk < BK / 16; ++kk) {
+            const uint64_t a = ad + (uint64_t)((kk * 32) >> 4), bb = bd + (uint64_t)((kk * 2048) >> 4);
+            if constexpr (PAIR)
+              mma_pair(acc, a, bb, IDESC, (k | kk) ? 1u : 0u);
+            else
+              mma(acc, a, bb, IDESC, (k | kk) ? 1u : 0u);
+          }
+          if constexpr (PAIR)
+            commit_pair(empty(s));
+          else
+            commit(empty(s));
           if (++s == STAGES) {
             s = 0;
             ph ^= 1;
           }
         }
-        commit(afull(b));
+        if constexpr (PAIR)
+          commit_pair(afull(b));
+        else
+          commit(afull(b));
       }
     }
   } else {
@@ -232,47 +349,104 @@ gemm_swiglu_kernel(const __grid_constant__ CUtensorMap map_x,
     const int q = warp & 3, row = q * 32 + lane;  // TMEM lane quarter = warp % 4
     const uint32_t lane_off = (uint32_t)(q * 32) << 16;
     int it = 0;
-    for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+    for (int t = unit; t < tiles; t += units, ++it) {
       const int b = it & 1;
       int m_i, n_i;
       tm.at(t, m_i, n_i);
       mbar_wait(afull(b), (uint32_t)((it >> 1) & 1));
       __syncwarp();
       fence_after();
-      const uint32_t acc = tmem + (uint32_t)(b * 256) + lane_off;
-      const int64_t grow = (int64_t)m_i * BM + row;
+      const uint32_t acc = tmem + (uint32_t)(b * BNT) + lane_off;
+      const int64_t grow = (int64_t)m_i * TM + rank * BM + row;
       const bool valid = grow < M;
-      uint4* dst = reinterpret_cast<uint4*>(act + grow * ld_act + (int64_t)n_i * 128);
+      if constexpr (MODE == SWIGLU) {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + grow * ld_out +
+                                              (int64_t)n_i * 128);
 #pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        uint32_t g[32], u[32];
-        ld32(acc + c * 32, g);
-        ld32(acc + 128 + c * 32, u);
-        ld_wait(g);  // waits for both loads
-        ld_wait(u);
-        if (valid) {
-          float a[32];
+        for (int c = 0; c < 4; ++c) {
+          uint32_t g[32], u[32];
+          ld32(acc + c * 32, g);
+          ld32(acc + 128 + c * 32, u);
+          ld_wait(g);  // waits for both loads
+          ld_wait(u);
+          if (valid) {
+            float a[32];
 #pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const float x = __uint_as_float(g[e]);
-            a[e] = x / (1.f + __expf(-x)) * __uint_as_float(u[e]);
+            for (int e = 0; e < 32; ++e) {
+              const float x = __uint_as_float(g[e]);
+              a[e] = x / (1.f + __expf(-x)) * __uint_as_float(u[e]);
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              dst[c * 4 + e] =
+                  make_uint4(pack(a[8 * e], a[8 * e + 1]), pack(a[8 * e + 2], a[8 * e + 3]),
+                             pack(a[8 * e + 4], a[8 * e + 5]), pack(a[8 * e + 6], a[8 * e + 7]));
           }
+        }
+      } else if constexpr (MODE == STORE) {
+        uint4* dst = reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + grow * ld_out +
+                                              (int64_t)n_i * BNT);
+#pragma unroll 1
+        for (int c = 0; c < BNT / 32; ++c) {
+          uint32_t v[32];
+          ld32(acc + c * 32, v);
+          ld_wait(v);
+          if (valid) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            dst[c * 4 + e] = make_uint4(pack(a[8 * e], a[8 * e + 1]), pack(a[8 * e + 2], a[8 * e + 3]),
-                                        pack(a[8 * e + 4], a[8 * e + 5]),
-                                        pack(a[8 * e + 6], a[8 * e + 7]));
+            for (int e = 0; e < 4; ++e)
+              dst[c * 4 + e] = make_uint4(
+                  pack(__uint_as_float(v[8 * e]), __uint_as_float(v[8 * e + 1])),
+                  pack(__uint_as_float(v[8 * e + 2]), __uint_as_float(v[8 * e + 3])),
+                  pack(__uint_as_float(v[8 * e + 4]), __uint_as_float(v[8 * e + 5])),
+                  pack(__uint_as_float(v[8 * e + 6]), __uint_as_float(v[8 * e + 7])));
+          }
+        }
+      } else {
+        float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + grow * ld_out +
+                                                (int64_t)n_i * BNT);
+#pragma unroll 1
+        for (int c = 0; c < BNT / 32; ++c) {
+          uint32_t v[32];
+          ld32(acc + c * 32, v);
+          float4 h[8];
+          if (valid) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e) h[e] = dst[c * 8 + e];
+          }
+          ld_wait(v);
+          if (valid) {
+#pragma unroll
+            for (int e = 0; e < 8; ++e)
+              dst[c * 8 + e] = make_float4(h[e].x + __uint_as_float(v[4 * e]),
+                                           h[e].y + __uint_as_float(v[4 * e + 1]),
+                                           h[e].z + __uint_as_float(v[4 * e + 2]),
+                                           h[e].w + __uint_as_float(v[4 * e + 3]));
+          }
         }
       }
       fence_before();
-      mbar_arrive(aempty(b));
+      __syncwarp();
+      if (lane == 0) {
+        if constexpr (PAIR)
+          mbar_arrive_leader(aempty(b));
+        else
+          mbar_arrive(aempty(b));
+      }
     }
   }
   fence_before();
-  __syncthreads();
+  if constexpr (PAIR)
+    cluster_sync();  // both CTAs done with TMEM and with each other's barriers
+  else
+    __syncthreads();
   if (warp == 1) {
     fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BNT)
+                   : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * BNT)
+                   : "memory");
   }
 }
 
@@ -323,34 +497,114 @@ static int sm_count() {
 
 using namespace ct;
 
-extern "C" int ct_gemm_swiglu(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
-                              int64_t I, int64_t ldw, void* act, int64_t ld_act, void* stream) {
-  if (M < 1 || K < 1 || I < 1)
-    return fail(CT_ERR_SHAPE, "gemm_swiglu geometry M=%lld K=%lld I=%lld", (long long)M,
-                (long long)K, (long long)I);
-  if (K % gm::BK || I % 128 || ldx < K || ldw < 2 * I || ld_act < I)
-    return fail(CT_ERR_UNSUPPORTED, "gemm_swiglu needs K %% 64 == 0, I %% 128 == 0 (K=%lld I=%lld)",
-                (long long)K, (long long)I);
-  if (!x || !w || !act) return fail(CT_ERR_PARAM, "null tensor");
-  if ((((uintptr_t)x | (uintptr_t)w | (uintptr_t)act) & 15) || ldx % 8 || ldw % 8 || ld_act % 8)
-    return fail(CT_ERR_UNSUPPORTED, "gemm_swiglu needs 16-byte aligned rows");
-  if (M > INT32_MAX / 2) return fail(CT_ERR_UNSUPPORTED, "M too large");
+namespace {
+
+template <int MODE, int BNT>
+int launch_mode(int ncta, const CUtensorMap& mx, const CUtensorMap& mw, void* out, int M, int N,
+                int K, int64_t ld_out, int band_m, int units, cudaStream_t stream) {
+  cudaLaunchConfig_t lc = {};
+  cudaLaunchAttribute at[1];
+  lc.gridDim = dim3((unsigned)(units * ncta));
+  lc.blockDim = dim3(192);
+  lc.stream = stream;
+  if (ncta == 2) {
+    CT_CUDA(cudaFuncSetAttribute(gm::gemm_kernel<2, MODE, BNT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gm::Cfg<2, BNT>::SMEM));
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    lc.dynamicSmemBytes = gm::Cfg<2, BNT>::SMEM;
+    CT_CUDA(cudaLaunchKernelEx(&lc, gm::gemm_kernel<2, MODE, BNT>, mx, mw, out, M, N, K, ld_out,
+                               band_m));
+  } else {
+    CT_CUDA(cudaFuncSetAttribute(gm::gemm_kernel<1, MODE, BNT>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)gm::Cfg<1, BNT>::SMEM));
+    lc.dynamicSmemBytes = gm::Cfg<1, BNT>::SMEM;
+    CT_CUDA(cudaLaunchKernelEx(&lc, gm::gemm_kernel<1, MODE, BNT>, mx, mw, out, M, N, K, ld_out,
+                               band_m));
+  }
+  return check_launch(MODE == gm::SWIGLU ? "gemm_swiglu_kernel" : "gemm_bf16_kernel");
+}
+
+// x [M][K] bf16 (row stride ldx) times w [K][wcols] bf16 (row stride ldw);
+// N = activation width (SWIGLU, wcols = 2N) or output columns (wcols = N)
+int launch(int mode, const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
+           int64_t wcols, int64_t ldw, int64_t N, void* out, int64_t ld_out, int out_bytes,
+           void* stream) {
+  if (M < 1 || K < 1 || N < 1)
+    return fail(CT_ERR_SHAPE, "gemm geometry M=%lld K=%lld N=%lld", (long long)M, (long long)K,
+                (long long)N);
+  if (K % gm::BK || N % 128 || ldx < K || ldw < wcols || ld_out < N)
+    return fail(CT_ERR_UNSUPPORTED, "gemm needs K %% 64 == 0 and N %% 128 == 0 (K=%lld N=%lld)",
+                (long long)K, (long long)N);
+  if (!x || !w || !out) return fail(CT_ERR_PARAM, "null tensor");
+  if ((((uintptr_t)x | (uintptr_t)w | (uintptr_t)out) & 15) || ldx % 8 || ldw % 8 ||
+      (ld_out * out_bytes) % 16)
+    return fail(CT_ERR_UNSUPPORTED, "gemm needs 16-byte aligned rows");
+  if (M > INT32_MAX / 2 || N > INT32_MAX / 4) return fail(CT_ERR_UNSUPPORTED, "gemm too large");
   CUtensorMap mx, mw;
   int rc;
   if ((rc = gm::map2d(&mx, x, (uint64_t)K, (uint64_t)M, (uint64_t)ldx, 64, gm::BM))) return rc;
-  if ((rc = gm::map2d(&mw, w, (uint64_t)(2 * I), (uint64_t)K, (uint64_t)ldw, 64, 64))) return rc;
-  CT_CUDA(cudaFuncSetAttribute(gm::gemm_swiglu_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)gm::SMEM));
-  const int64_t tiles = ((M + gm::BM - 1) / gm::BM) * (I / 128);
-  const unsigned grid = (unsigned)std::min<int64_t>(tiles, gm::sm_count());
+  if ((rc = gm::map2d(&mw, w, (uint64_t)wcols, (uint64_t)K, (uint64_t)ldw, 64, 64))) return rc;
+  // CT_GEMM_1SM=1 (read once): the single-SM form, for A/B
+  static const bool one_sm = [] {
+    const char* e = getenv("CT_GEMM_1SM");
+    return e && e[0] == '1';
+  }();
+  const int ncta = one_sm ? 1 : 2;
+  const int64_t tm_rows = (int64_t)gm::BM * ncta;
+  const int64_t mt = (M + tm_rows - 1) / tm_rows, slots = gm::sm_count() / ncta;
+  // tile width (accumulator columns): 256 (SWIGLU: 128 gate + 128 up).
+  // 128-wide tiles only when N % 256 != 0: at N = 128 each MMA still reads
+  // the whole A operand from shared memory for half the MACs, and measured
+  // 25-33 % slower than 256-wide tiles on the step's projections even where
+  // they fill the last wave better (tools/gemm_proj_bench.py)
+  const bool narrow = mode != gm::SWIGLU && N % 256;
+  const int64_t tiles = mt * (mode == gm::SWIGLU ? N / 128 : N / (narrow ? 128 : 256));
   // M-tiles per band: an A slice of at most ~60 MB (L2 is 126 MB over two
-  // dies; a single 81 MB band measured 4 % slower than two), bands of
-  // equal size
-  const int64_t mt = (M + gm::BM - 1) / gm::BM;
-  const int64_t fit = std::max<int64_t>(1, (int64_t)60e6 / (gm::BM * K * 2));
+  // dies), bands of equal size.  Standalone (tools/gemm_band_sweep.sh) 40
+  // and 60 MB tie at 2K / 5K / 10K rows and 40 MB wins at 32K rows (one band
+  // -26 %); inside the power-capped step 60 MB measured 0.4-0.5 ms faster
+  // per request at configs 2 and 3 (config 2's 41 MB x stays one band, so W
+  // is read from HBM once instead of twice), and the step's fused calls stay
+  // below 16K rows
+  static const int64_t band_bytes = [] {  // CT_GEMM_BAND_MB (read once): sweep switch
+    const char* e = getenv("CT_GEMM_BAND_MB");
+    return (int64_t)((e && atoi(e) > 0) ? atoi(e) : 60) * 1000000;
+  }();
+  const int64_t fit = std::max<int64_t>(1, band_bytes / (tm_rows * K * 2));
   const int64_t nbands = (mt + fit - 1) / fit;
   const int band_m = (int)((mt + nbands - 1) / nbands);
-  gm::gemm_swiglu_kernel<<<grid, 192, gm::SMEM, (cudaStream_t)stream>>>(
-      mx, mw, (__nv_bfloat16*)act, (int)M, (int)I, (int)K, ld_act, band_m);
-  return check_launch("gemm_swiglu_kernel");
+  const int units = (int)std::min<int64_t>(tiles, slots);
+  const cudaStream_t st = (cudaStream_t)stream;
+  const int m = (int)M, n = (int)N, k = (int)K;
+  if (mode == gm::SWIGLU)
+    return launch_mode<gm::SWIGLU, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st);
+  if (mode == gm::STORE)
+    return narrow ? launch_mode<gm::STORE, 128>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st)
+                  : launch_mode<gm::STORE, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st);
+  return narrow ? launch_mode<gm::ADD, 128>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st)
+                : launch_mode<gm::ADD, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st);
+}
+
+}  // namespace
+
+extern "C" int ct_gemm_swiglu(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
+                              int64_t I, int64_t ldw, void* act, int64_t ld_act, void* stream) {
+  return launch(gm::SWIGLU, x, M, K, ldx, w, 2 * I, ldw, I, act, ld_act, 2, stream);
+}
+
+extern "C" int ct_gemm_bf16(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
+                            int64_t N, int64_t ldw, void* out, int64_t ld_out, int out_dtype,
+                            int accumulate, void* stream) {
+  if (out_dtype == CT_BF16 && !accumulate)
+    return launch(gm::STORE, x, M, K, ldx, w, N, ldw, N, out, ld_out, 2, stream);
+  if (out_dtype == CT_F32 && accumulate)
+    return launch(gm::ADD, x, M, K, ldx, w, N, ldw, N, out, ld_out, 4, stream);
+  return fail(CT_ERR_UNSUPPORTED, "gemm_bf16: bf16 store or f32 accumulate only");
 }

@@ -3,8 +3,10 @@
 `selective_prefill` keeps the reference's signature, validation and result
 fields; `full_prefill` is the baseline and r=1 oracle; `encode_chunk_isolated`
 produces the pre-RoPE chunk KV (the offline producer).  Per layer the engine
-runs (all on the current CUDA stream, every op a libcachetune_b200 kernel
-except the dense projections, which are cuBLAS via torch.mm):
+runs (all on the current CUDA stream, every op a libcachetune_b200 kernel;
+in the bf16 step the dense projections run on the library's CTA-pair tcgen05
+GEMM (ct_gemm_swiglu for gate/up + SwiGLU, ct_gemm_bf16 for QKV / O / down)
+where it measured faster, else on cuBLAS via torch.mm):
 
   K4  ct_qkv_rope_scatter   q,k RoPE at active positions; k,v -> cache rows
   K3  ct_gather_rope_blend  reused rows -> cache rows, K rotated at global pos
@@ -127,13 +129,13 @@ def _record_mode(record):
 # CT_MLP_FUSED=0 (read once) keeps the bf16 SwiGLU MLP on cuBLAS + ct_mlp_act
 # (the A/B baseline of the fused tcgen05 gate/up kernel)
 _MLP_FUSED_ENV = __import__("os").environ.get("CT_MLP_FUSED", "1") != "0"
-# row range of the fused kernel, from end-to-end A/B (CT_MLP_FUSED=0/1):
-# below 128 rows a tile is mostly padding; at config 2's 4,992 active rows it
-# saves 2.8 ms per request (96.1 -> 93.3 ms); at 9,920 rows (config 3) it is
-# neutral to 0.5 % slower and at 32K rows (full prefill) 3.5 % slower than
-# cuBLAS's two-CTA 256 x 256 tiles + the separate SwiGLU kernel, so larger
-# calls keep that path and each path runs its faster implementation
-FUSED_MIN_ROWS, FUSED_MAX_ROWS = 128, 8192
+# row range of the fused kernel (CTA-pair tcgen05 GEMM), from end-to-end A/B
+# (tools/mlp_fused_ab.sh, CT_MLP_FUSED=0/1): below 128 rows a tile is mostly
+# padding; config 2's 4,992 active rows 95.0 -> 93.1 ms per request, config
+# 3's 9,920 rows 256.1 -> 252.6 ms; the 32K / 64K-row full prefill is neutral
+# to 0.5 % slower fused (sustained power-capped clocks), so the baseline keeps
+# cuBLAS + the activation kernel there and each path runs its faster form
+FUSED_MIN_ROWS, FUSED_MAX_ROWS = 128, 16384
 
 
 def _fused_mlp(model: GpuModel) -> bool:
@@ -173,12 +175,53 @@ def _mm_f32(a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
     return torch.mm(a, w, out_dtype=torch.float32)
 
 
-def _residual_mm(h: torch.Tensor, a: torch.Tensor, w: torch.Tensor) -> None:
-    """h += a @ w in the GEMM epilogue (cuBLAS beta = 1, f32 C/D, bf16 or f32
-    A/B): the residual add of ct/toymodel.py:184,189 without a separate f32
-    delta round trip through HBM."""
+# CT_GEMM_OWN=1 (read once) runs the bf16 QKV / O / down projections on
+# ct_gemm_bf16 where `_own_gemm` picks it.  Off by default: standalone it is
+# up to 19 % faster than cuBLAS, but inside the power-capped step it lowered
+# the SM clock (1,470 vs 1,505 MHz) and measured neutral at config 2 (94.9 vs
+# 94.9 ms) and 1 % slower at config 3 (261.5 vs 258.8 ms)
+_GEMM_OWN_ENV = __import__("os").environ.get("CT_GEMM_OWN", "0") == "1"
+_PAIRS = []
+
+
+def _own_gemm(a: torch.Tensor, w: torch.Tensor) -> bool:
+    """Run a bf16 projection on ct_gemm_bf16 (CTA-pair tcgen05, 256 x 256
+    tiles) when its tiles fill >= 90 % of the last wave of the 74 SM pairs,
+    else cuBLAS.  tools/gemm_proj_bench.py, ours vs cuBLAS: 9,920 rows (config
+    3) QKV / O / down +5 / +11 / +19 % (94-97 % filled); 4,992 rows (config 2)
+    QKV +3 % (93 %), O / down -4 / -12 % (320 tiles = 86 % filled, cuBLAS
+    kept).  Same row range as the fused MLP."""
+    rows, k = a.shape
+    n = w.shape[1]
+    if not (_GEMM_OWN_ENV and a.dtype == torch.bfloat16 and w.dtype == torch.bfloat16
+            and FUSED_MIN_ROWS <= rows <= FUSED_MAX_ROWS and n % 256 == 0 and k % 64 == 0
+            and a.stride(1) == 1 and w.stride(1) == 1):
+        return False
+    if not _PAIRS:
+        _PAIRS.append(torch.cuda.get_device_properties(a.device).multi_processor_count // 2)
+    tiles = -(-rows // 256) * (n // 256)
+    return tiles / (-(-tiles // _PAIRS[0]) * _PAIRS[0]) >= 0.9
+
+
+def _proj_mm(out: torch.Tensor, a: torch.Tensor, w: torch.Tensor, st) -> None:
+    """out = a @ w (the QKV projection, ct/toymodel.py:176)."""
+    if _own_gemm(a, w):
+        _lib.call("ct_gemm_bf16", _dev.ptr(a), a.shape[0], a.shape[1], a.stride(0), _dev.ptr(w),
+                  w.shape[1], w.stride(0), _dev.ptr(out), out.stride(0), _lib.CT_BF16, 0, st)
+    else:
+        torch.mm(a, w, out=out)
+
+
+def _residual_mm(h: torch.Tensor, a: torch.Tensor, w: torch.Tensor, st=None) -> None:
+    """h += a @ w in the GEMM epilogue (f32 C/D, bf16 or f32 A/B): the
+    residual add of ct/toymodel.py:184,189 without a separate f32 delta round
+    trip through HBM.  ct_gemm_bf16 (accumulate) where `_own_gemm` picks it,
+    else cuBLAS beta = 1."""
     if a.dtype == torch.float32:
         h.addmm_(a, w)
+    elif st is not None and _own_gemm(a, w):
+        _lib.call("ct_gemm_bf16", _dev.ptr(a), a.shape[0], a.shape[1], a.stride(0), _dev.ptr(w),
+                  w.shape[1], w.stride(0), _dev.ptr(h), h.stride(0), _lib.CT_F32, 1, st)
     else:
         torch.ops.aten.addmm.dtype_out(h, a, w, torch.float32, beta=1, alpha=1, out=h)
 
@@ -235,7 +278,7 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
         kc, vc = caches[l]
         if hook is not None:
             hook(l, "start")
-        torch.mm(buf.x, w["wqkv"], out=buf.qkv)
+        _proj_mm(buf.qkv, buf.x, w["wqkv"], st)
         tq = timer.start("qkv") if timer is not None else None
         _lib.check(lib.ct_qkv_rope_scatter(
             _dev.ptr(buf.qkv), buf.qkv.shape[1], dtc, _dev.ptr(positions), a, hq, hkv, d,
@@ -288,7 +331,7 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
                 _dev.ptr(scratch), dtc, _dev.ptr(part), _dev.ptr(_dev.workspace(wsr, "record")),
                 wsr, st), "ct_selective_attention")
             probs_all.append(part)
-        _residual_mm(hv, ctxv, w["wo"])
+        _residual_mm(hv, ctxv, w["wo"], st)
         _lib.call("ct_residual_rmsnorm", _dev.ptr(hv), None, _lib.CT_F32, av, hid,
                   NORM_EPS, _dev.ptr(xv), dtc, st)
         kind = cfg.mlp_kind
@@ -306,7 +349,7 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
                 torch.mm(xv, up, out=guv)
                 _lib.call("ct_mlp_act", _dev.ptr(guv), av, inter, dtc,
                           1 if kind == "relu" else 0, _dev.ptr(actv), dtc, st)
-            _residual_mm(hv, actv, down)
+            _residual_mm(hv, actv, down, st)
             _lib.call("ct_residual_rmsnorm", _dev.ptr(hv), None, _lib.CT_F32, av,
                       hid, NORM_EPS, _dev.ptr(xv), dtc, st)
         if hook is not None:
