@@ -282,14 +282,14 @@ int ct_mlp_act(const void* gu, int64_t A, int64_t inter, int in_dtype,
                int kind, void* act, int act_dtype, void* stream);
 
 /* act[m][i] = silu(g) * u with g = (x @ w)[m][i], u = (x @ w)[m][I + i]: the
- * SwiGLU gate/up projection and activation of ct/toymodel.py:184-186 in one
+ * SwiGLU gate/up projection and activation (ct/toymodel.py:186, w1 + act) in one
  * tcgen05 kernel (bf16 x [M][K] row stride ldx, w [K][2I] row stride ldw,
  * act [M][I] row stride ld_act; f32 accumulation, the [M][2I] product never
  * stored).  K % 64 == 0, I % 128 == 0, 16-byte aligned rows. */
 int ct_gemm_swiglu(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
                    int64_t I, int64_t ldw, void* act, int64_t ld_act, void* stream);
 
-/* The dense projections of the bf16 step (ct/toymodel.py:176-189) on the
+/* The dense projections of the bf16 step (ct/toymodel.py:157-159,184,186) on the
  * same CTA-pair tcgen05 GEMM: x bf16 [M][K] (row stride ldx) times w bf16
  * [K][N] (row stride ldw), f32 accumulation, and
  *   out_dtype CT_BF16, accumulate 0: out bf16 [M][N]  = x @ w   (QKV)

@@ -1,7 +1,7 @@
 // Gate/up projection with the SwiGLU activation fused into the epilogue, on
 // the 5th-gen tensor cores (sm_100a).  Replaces, for the bf16 step, the pair
 //     gu = x @ W_gu (cuBLAS)   ->   act = silu(gu[:, :I]) * gu[:, I:]  (ct_mlp_act)
-// of ct/toymodel.py:184-186 (the SwiGLU MLP of the restated Llama/Mistral
+// of ct/toymodel.py:186 (the MLP, as SwiGLU in the restated Llama/Mistral
 // geometry): the [M, 2I] gate/up product never reaches HBM, and the
 // activation is computed from the f32 accumulators.
 //

@@ -204,7 +204,7 @@ def _own_gemm(a: torch.Tensor, w: torch.Tensor) -> bool:
 
 
 def _proj_mm(out: torch.Tensor, a: torch.Tensor, w: torch.Tensor, st) -> None:
-    """out = a @ w (the QKV projection, ct/toymodel.py:176)."""
+    """out = a @ w (the q / k / v projections, ct/toymodel.py:157-159)."""
     if _own_gemm(a, w):
         _lib.call("ct_gemm_bf16", _dev.ptr(a), a.shape[0], a.shape[1], a.stride(0), _dev.ptr(w),
                   w.shape[1], w.stride(0), _dev.ptr(out), out.stride(0), _lib.CT_BF16, 0, st)
@@ -214,7 +214,7 @@ def _proj_mm(out: torch.Tensor, a: torch.Tensor, w: torch.Tensor, st) -> None:
 
 def _residual_mm(h: torch.Tensor, a: torch.Tensor, w: torch.Tensor, st=None) -> None:
     """h += a @ w in the GEMM epilogue (f32 C/D, bf16 or f32 A/B): the
-    residual add of ct/toymodel.py:184,189 without a separate f32 delta round
+    residual add of ct/toymodel.py:184,186 without a separate f32 delta round
     trip through HBM.  ct_gemm_bf16 (accumulate) where `_own_gemm` picks it,
     else cuBLAS beta = 1."""
     if a.dtype == torch.float32:

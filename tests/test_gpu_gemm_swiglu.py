@@ -1,6 +1,6 @@
 """ct_gemm_swiglu (tcgen05 gate/up projection with the SwiGLU activation in
 the epilogue) against a PyTorch fp32 reference of the same op,
-silu(x @ Wg) * (x @ Wu) (ct/toymodel.py:184-186), on bf16 operands: ragged
+silu(x @ Wg) * (x @ Wu) (the MLP of ct/toymodel.py:186 as SwiGLU), on bf16 operands: ragged
 row counts (tail tiles), small and config-2 widths, strided rows."""
 
 import pytest
