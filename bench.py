@@ -514,6 +514,7 @@ def run_ours(args, rank, world, local_rank):
     att_ms = timer.mean_ms("attention")
     blend_ms = timer.mean_ms("blend")
     qkv_ms = timer.mean_ms("qkv")
+    mlp_ms = timer.mean_ms("mlp_gemm")  # nan when the fused MLP does not run
     # ---- e2e: pinned host pool, H2D keep rows + tokens, D2H logits, all timed
     e2e_ms, e2e_total = timed(lambda: eng_e2e.step(suffix_host, logits_host), args.steps)
     # sparse transfer alone (copy engines, after the timed regions): one
@@ -568,6 +569,7 @@ def run_ours(args, rank, world, local_rank):
     att_ms = allmax(att_ms)
     blend_ms = allmax(blend_ms)
     qkv_ms = allmax(qkv_ms)
+    mlp_ms = allmax(mlp_ms)
     sc64 = allmax(sc_times["f64"])
     scfast = allmax(sc_times["fast"])
     if rank != 0:
@@ -578,6 +580,9 @@ def run_ours(args, rank, world, local_rank):
     L = cfg.n_layers
     att_flops = eng.attention_flops_per_layer()
     att_tflops = att_flops / (att_ms * 1e-3) / 1e12
+    mlp_flops = 2.0 * eng.A * cfg.hidden_dim * 2 * cfg.inter
+    # x read + W_gu read + act written (bf16)
+    mlp_floor = 2 * (eng.A * cfg.hidden_dim + cfg.hidden_dim * 2 * cfg.inter + eng.A * cfg.inter)
     blend_bytes = eng.blend_bytes_per_layer()
     blend_gbs = blend_bytes / (blend_ms * 1e-3) / 1e9
     # QKV epilogue: read q|k|v rows, write q + cache K + cache V (+ no raw K here)
@@ -653,6 +658,15 @@ def run_ours(args, rank, world, local_rank):
                                  "unit": "GB/s", "frac": qkv_gbs / peaks["hbm"],
                                  "bytes_per_launch": qkv_bytes, "launch_ms": qkv_ms,
                                  "traffic": ncu_traffic("qkv_bf16_kernel", args.config)},
+            # MLP gate/up GEMM + SwiGLU epilogue (ct_gemm_swiglu, tcgen05 CTA
+            # pairs): 2 A hid 2I flops per launch, timed per launch in-step
+            "mlp_gate_up_swiglu": (None if not np.isfinite(mlp_ms) else {
+                "bound": "tensor", "achieved": mlp_flops / (mlp_ms * 1e-3) / 1e12,
+                "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
+                "frac": mlp_flops / (mlp_ms * 1e-3) / 1e12 / peaks["bf16_sust"],
+                "flops_per_launch": mlp_flops, "launch_ms": mlp_ms,
+                "hbm_floor_bytes": mlp_floor,
+                "traffic": ncu_traffic("gemm_swiglu_kernel", args.config)}),
             "scorer_f64_per_request": {
                 "ms": sc64, "bytes": scorer_bytes, "bound": "fp64 (exact mode)",
                 "hbm_gbs": scorer_bytes / (sc64 * 1e-3) / 1e9,

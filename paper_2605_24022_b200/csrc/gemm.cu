@@ -67,13 +67,31 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t b, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(b) : "memory");
 }
+// try_wait suspend-time hint (ns): waiting threads (4 epilogue warps, the
+// producer and the MMA thread per CTA) may sleep instead of re-issuing the
+// poll.  In-step A/B (tools/gemm_power_ab.sh, profiles/round2_gemm_power_ab.txt):
+// -0.3 to -0.5 ms per request at configs 2 and 3 under the power cap.
+// -DCT_GEMM_SUSPEND_NS=0 builds the plain spin.
+#ifndef CT_GEMM_SUSPEND_NS
+#define CT_GEMM_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t b, uint32_t par) {
+#if CT_GEMM_SUSPEND_NS
+  // waiting threads may be suspended up to the hint instead of re-issuing
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tLW:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra LD;\n\tbra LW;\n\tLD:\n\t}" ::"r"(b),
+      "r"(par), "n"(CT_GEMM_SUSPEND_NS)
+      : "memory");
+#else
   asm volatile(
       "{\n\t.reg .pred P1;\n\tLW:\n\t"
       "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
       "@P1 bra LD;\n\tbra LW;\n\tLD:\n\t}" ::"r"(b),
       "r"(par)
       : "memory");
+#endif
 }
 __device__ __forceinline__ void tma2d(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0,
                                       int c1) {

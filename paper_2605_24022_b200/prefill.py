@@ -342,8 +342,11 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
             inter = buf.act.shape[1]
             if (kind == "swiglu" and FUSED_MIN_ROWS <= av <= FUSED_MAX_ROWS
                     and _fused_mlp(model)):
+                tg = timer.start("mlp_gemm") if timer is not None else None
                 _lib.call("ct_gemm_swiglu", _dev.ptr(xv), av, hid, xv.stride(0), _dev.ptr(up),
                           inter, up.stride(0), _dev.ptr(actv), actv.stride(0), st)
+                if timer is not None:
+                    timer.stop("mlp_gemm", tg)
             else:
                 guv = buf.gu[:av]
                 torch.mm(xv, up, out=guv)
