@@ -143,7 +143,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------------------------- CPU arm
 
-def cpu_sample(cfgname: str, seed: int = 0, rows: int = 32):
+def cpu_sample(cfgname: str, seed: int = 0, rows: int = 256):
     """Bounded sample of the reference CPU path (oracle port, float64 numpy):
     one layer of config `cfgname` for `rows` active query rows (uniformly spread
     over the request's real positions) + that layer's full deferred-RoPE fuse,
@@ -960,7 +960,7 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--no-full", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-rows", type=int, default=32)
+    ap.add_argument("--cpu-rows", type=int, default=256)
     ap.add_argument("--resident-layers", type=int, default=0,
                     help="e2e arm: first n layers of the pinned pool also kept in HBM")
     ap.add_argument("--side-configs", default="auto", choices=["auto", "none"],
