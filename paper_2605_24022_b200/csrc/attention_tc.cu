@@ -59,7 +59,28 @@ __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+// try_wait with a suspend-time hint (ns): waiting warps may sleep instead of
+// re-issuing the poll, as gemm.cu's CT_GEMM_SUSPEND_NS.  A/B vs the plain spin
+// (tools/att_suspend_ab.sh, profiles/round2_attention_suspend_ab.txt): outputs
+// bit-identical, in-step launch -0.3 % (config 2) / -0.7 % (config 3), p50
+// -0.1 / -0.8 ms per request, every rep; a 2 us hint is neutral to slower.
+// -DCT_TC_SUSPEND_NS=0 builds the plain spin.
+#ifndef CT_TC_SUSPEND_NS
+#define CT_TC_SUSPEND_NS 1000000
+#endif
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+#if CT_TC_SUSPEND_NS
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "LAB_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+      "@P1 bra DONE;\n\t"
+      "bra LAB_WAIT;\n\t"
+      "DONE:\n\t}" ::"r"(bar),
+      "r"(parity), "n"(CT_TC_SUSPEND_NS)
+      : "memory");
+  return;
+#endif
   asm volatile(
       "{\n\t.reg .pred P1;\n\t"
       "LAB_WAIT:\n\t"
