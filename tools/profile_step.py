@@ -26,7 +26,8 @@ from paper_2605_24022_b200.spectral import score_device  # noqa: E402
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--what", default="step", choices=["step", "scorer", "scorer32", "full"])
+    ap.add_argument("--what", default="step",
+                    choices=["step", "scorer", "scorer32", "full", "busy"])
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--chunks", type=int, default=16)
     args = ap.parse_args()
@@ -65,10 +66,49 @@ def main():
     eng = SelectivePrefillEngine(model, pool, 0.15, 64)
     eng.step(suffix)
     torch.cuda.synchronize()
+    if args.what == "busy":
+        busy(eng, suffix)
+        return
     torch.cuda.profiler.start()
     eng.step(suffix)
     torch.cuda.synchronize()
     torch.cuda.profiler.stop()
+
+
+def busy(eng, suffix, steps: int = 3):
+    """GPU busy fraction of back-to-back requests at full concurrency (CUPTI
+    kernel + memcpy intervals via torch.profiler, not serialised like ncu):
+    the union of device intervals vs the span from the first start to the
+    last end, and the largest idle gaps with the activity that follows."""
+    from torch.profiler import ProfilerActivity, profile
+    for _ in range(2):
+        eng.step(suffix)
+    torch.cuda.synchronize()
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        for _ in range(steps):
+            eng.step(suffix)
+        torch.cuda.synchronize()
+    ev = sorted(((e.time_range.start, e.time_range.end, e.name) for e in prof.events()
+                 if e.device_type.name == "CUDA"), key=lambda x: x[0])
+    if not ev:
+        print("no device activity recorded")
+        return
+    t0, t1 = ev[0][0], max(e[1] for e in ev)
+    busy_us, cur_s, cur_e, gaps = 0.0, ev[0][0], ev[0][1], []
+    for s, e, n in ev[1:]:
+        if s > cur_e:
+            busy_us += cur_e - cur_s
+            gaps.append((s - cur_e, n))
+            cur_s, cur_e = s, e
+        else:
+            cur_e = max(cur_e, e)
+    busy_us += cur_e - cur_s
+    span = t1 - t0
+    print(f"{steps} requests: span {span / 1e3:.3f} ms, device busy {busy_us / 1e3:.3f} ms "
+          f"({100 * busy_us / span:.1f} %), idle {(span - busy_us) / 1e3:.3f} ms in "
+          f"{len(gaps)} gaps")
+    for g, n in sorted(gaps, reverse=True)[:15]:
+        print(f"  gap {g:9.1f} us before {n[:90]}")
 
 
 if __name__ == "__main__":
