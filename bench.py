@@ -515,6 +515,7 @@ def run_ours(args, rank, world, local_rank):
     blend_ms = timer.mean_ms("blend")
     qkv_ms = timer.mean_ms("qkv")
     mlp_ms = timer.mean_ms("mlp_gemm")  # nan when the fused MLP does not run
+    qkvg_ms = timer.mean_ms("qkv_gemm")  # nan when the fused QKV GEMM does not run
     # ---- e2e: pinned host pool, H2D keep rows + tokens, D2H logits, all timed
     e2e_ms, e2e_total = timed(lambda: eng_e2e.step(suffix_host, logits_host), args.steps)
     # ---- the same requests replayed from CUDA graphs (the engines' public
@@ -597,6 +598,7 @@ def run_ours(args, rank, world, local_rank):
     blend_ms = allmax(blend_ms)
     qkv_ms = allmax(qkv_ms)
     mlp_ms = allmax(mlp_ms)
+    qkvg_ms = allmax(qkvg_ms)
     sc64 = allmax(sc_times["f64"])
     scfast = allmax(sc_times["fast"])
     if rank != 0:
@@ -615,6 +617,7 @@ def run_ours(args, rank, world, local_rank):
     # QKV epilogue: read q|k|v rows, write q + cache K + cache V (+ no raw K here)
     qkv_bytes = 2 * eng.A * (cfg.n_heads + 2 * cfg.kv_heads) * cfg.head_dim * 2
     qkv_gbs = qkv_bytes / (qkv_ms * 1e-3) / 1e9
+    qkvg_flops = 2.0 * eng.A * cfg.hidden_dim * (cfg.n_heads + 2 * cfg.kv_heads) * cfg.head_dim
     # scorer: exact mode is FP64-pipe bound.  Algorithmic work = a forward and
     # an inverse complex FFT (split-radix 4N log2 N - 6N + 8 flops) per packed
     # pair of lanes; peak = 64 DFMA lanes/clk/SM x 2 x 148 SMs x max SM clock.
@@ -681,10 +684,20 @@ def run_ours(args, rank, world, local_rank):
                                   "unit": "GB/s", "frac": blend_gbs / peaks["hbm"],
                                   "bytes_per_launch": blend_bytes, "launch_ms": blend_ms,
                                   "traffic": ncu_traffic("blend_bf16_kernel", args.config)},
-            "qkv_rope_scatter": {"bound": "hbm", "achieved": qkv_gbs, "peak": peaks["hbm"],
-                                 "unit": "GB/s", "frac": qkv_gbs / peaks["hbm"],
-                                 "bytes_per_launch": qkv_bytes, "launch_ms": qkv_ms,
-                                 "traffic": ncu_traffic("qkv_bf16_kernel", args.config)},
+            # separate QKV epilogue kernel: only when the fused QKV GEMM is off
+            "qkv_rope_scatter": (None if not np.isfinite(qkv_ms) else {
+                "bound": "hbm", "achieved": qkv_gbs, "peak": peaks["hbm"],
+                "unit": "GB/s", "frac": qkv_gbs / peaks["hbm"],
+                "bytes_per_launch": qkv_bytes, "launch_ms": qkv_ms,
+                "traffic": ncu_traffic("qkv_bf16_kernel", args.config)}),
+            # q|k|v GEMM with RoPE + cache scatter in the epilogue
+            # (ct_gemm_qkv_rope): 2 A hid (Hq + 2 Hkv) D flops per launch
+            "qkv_gemm_rope": (None if not np.isfinite(qkvg_ms) else {
+                "bound": "tensor", "achieved": qkvg_flops / (qkvg_ms * 1e-3) / 1e12,
+                "peak": peaks["bf16_sust"], "unit": "TFLOP/s",
+                "frac": qkvg_flops / (qkvg_ms * 1e-3) / 1e12 / peaks["bf16_sust"],
+                "flops_per_launch": qkvg_flops, "launch_ms": qkvg_ms,
+                "traffic": ncu_traffic("gemm_qkv_rope_kernel", args.config)}),
             # MLP gate/up GEMM + SwiGLU epilogue (ct_gemm_swiglu, tcgen05 CTA
             # pairs): 2 A hid 2I flops per launch, timed per launch in-step
             "mlp_gate_up_swiglu": (None if not np.isfinite(mlp_ms) else {

@@ -302,6 +302,21 @@ int ct_gemm_bf16(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w
                  int64_t ldw, void* out, int64_t ld_out, int out_dtype, int accumulate,
                  void* stream);
 
+/* The q|k|v projection with the K4 epilogue (ct_qkv_rope_scatter) fused, for
+ * the bf16 step with head_dim 128 and adjacent RoPE pairs
+ * (ct/toymodel.py:157-163, ct/rope.py:40-70): qkv = x @ w (w bf16
+ * [K][(Hq + 2 Hkv) 128], row stride ldw) in f32 accumulators, then q heads
+ * rotated at positions[m] -> q_out bf16 [M][Hq][128]; k heads rotated ->
+ * k_cache row positions[m]; v heads -> v_cache row positions[m] (row stride
+ * cache_row_stride elements).  table = the f32 (cos, sin) pair table
+ * [n_ctx][64] of ct_rope_table.  The [M][N] product never reaches HBM.
+ * K % 64 == 0, Hq + 2 Hkv even, 16-byte aligned rows; D != 128 returns
+ * CT_ERR_UNSUPPORTED. */
+int ct_gemm_qkv_rope(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
+                     int64_t ldw, const int32_t* positions, const void* table, int64_t Hq,
+                     int64_t Hkv, int64_t D, void* q_out, void* k_cache, void* v_cache,
+                     int64_t cache_row_stride, void* stream);
+
 /* ------------------------------------------------------------------ */
 /* (2) sparse pinned-host -> HBM transfer on the copy engines
  * (ct/cachepool.py:409-481 with an importance-ordered pool so each

@@ -105,6 +105,9 @@ _SIGS = {
                                c_void_p, c_int64, c_void_p]),
     "ct_gemm_bf16": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64, c_int64,
                              c_void_p, c_int64, c_int, c_int, c_void_p]),
+    "ct_gemm_qkv_rope": (c_int, [c_void_p, c_int64, c_int64, c_int64, c_void_p, c_int64,
+                                 c_void_p, c_void_p, c_int64, c_int64, c_int64, c_void_p,
+                                 c_void_p, c_void_p, c_int64, c_void_p]),
     "ct_copy_ranges_h2d": (c_int, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p]),
     "ct_host_alloc": (c_int, [ctypes.POINTER(c_void_p), c_size_t]),
     "ct_host_free": (c_int, [c_void_p]),

@@ -217,12 +217,27 @@ struct TileMap {
 // epilogues: SWIGLU act = silu(g) * u (bf16, B columns = gate | up halves of
 // width I); STORE out = x @ w (bf16); ADD out += x @ w (f32 residual, the
 // beta = 1 GEMM of the O- and down-projections)
-enum Mode { SWIGLU = 0, STORE = 1, ADD = 2 };
+// QKV: the q|k|v projection with the K4 epilogue of ct_qkv_rope_scatter
+// fused (bf16, head_dim 128, adjacent RoPE pairs): q heads rotated at the
+// row's position -> q_out [M, Hq, 128]; k heads rotated -> k cache row pos;
+// v heads -> v cache row pos.  RoPE runs on the f32 accumulators.
+enum Mode { SWIGLU = 0, STORE = 1, ADD = 2, QKV = 3 };
+
+struct QkvEpi {
+  const int32_t* pos;     // [M] global positions of the rows
+  const float4* table;    // [n_ctx][64] (cos, sin) f32 pairs, read as float4
+  __nv_bfloat16* q;       // [M][hq][128]
+  __nv_bfloat16* kc;      // cache rows [n_ctx] x crs
+  __nv_bfloat16* vc;
+  int64_t crs;
+  int hq, hkv;
+};
 
 template <int NCTA, int MODE, int BNT>
 __global__ void __launch_bounds__(192, 1)
 gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ CUtensorMap map_w,
-            void* __restrict__ out, int M, int N, int K, int64_t ld_out, int band_m) {
+            void* __restrict__ out, int M, int N, int K, int64_t ld_out, int band_m,
+            const QkvEpi qe) {
   // N: activation width I (SWIGLU) or output columns
   static_assert(MODE != SWIGLU || BNT == 256, "SWIGLU tiles pair 128 gate + 128 up columns");
   using C = Cfg<NCTA, BNT>;
@@ -419,6 +434,44 @@ gemm_kernel(const __grid_constant__ CUtensorMap map_x, const __grid_constant__ C
                   pack(__uint_as_float(v[8 * e + 6]), __uint_as_float(v[8 * e + 7])));
           }
         }
+      } else if constexpr (MODE == QKV) {
+        const int64_t pos = valid ? (int64_t)__ldg(qe.pos + grow) : 0;
+#pragma unroll 1
+        for (int c = 0; c < BNT / 32; ++c) {
+          uint32_t v[32];
+          ld32(acc + c * 32, v);
+          ld_wait(v);
+          if (valid) {
+            const int col = n_i * BNT + c * 32;
+            const int head = col >> 7, d0 = col & 127;
+            uint4* dst;
+            uint32_t pk[16];
+            if (head < qe.hq + qe.hkv) {
+              dst = reinterpret_cast<uint4*>(
+                  head < qe.hq ? qe.q + grow * (int64_t)qe.hq * 128 + col
+                               : qe.kc + pos * qe.crs + (head - qe.hq) * 128 + d0);
+              // 16 adjacent pairs (2j, 2j+1), j = d0/2 + e: 8 float4 of (cos, sin)
+              const float4* t = qe.table + pos * 32 + d0 / 4;
+#pragma unroll
+              for (int e = 0; e < 8; ++e) {
+                const float4 cs = __ldg(t + e);
+                const float x0 = __uint_as_float(v[4 * e]), y0 = __uint_as_float(v[4 * e + 1]);
+                const float x1 = __uint_as_float(v[4 * e + 2]), y1 = __uint_as_float(v[4 * e + 3]);
+                pk[2 * e] = pack(x0 * cs.x - y0 * cs.y, x0 * cs.y + y0 * cs.x);
+                pk[2 * e + 1] = pack(x1 * cs.z - y1 * cs.w, x1 * cs.w + y1 * cs.z);
+              }
+            } else {
+              dst = reinterpret_cast<uint4*>(qe.vc + pos * qe.crs +
+                                             (head - qe.hq - qe.hkv) * 128 + d0);
+#pragma unroll
+              for (int e = 0; e < 16; ++e)
+                pk[e] = pack(__uint_as_float(v[2 * e]), __uint_as_float(v[2 * e + 1]));
+            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              dst[e] = make_uint4(pk[4 * e], pk[4 * e + 1], pk[4 * e + 2], pk[4 * e + 3]);
+          }
+        }
       } else {
         float4* dst = reinterpret_cast<float4*>(static_cast<float*>(out) + grow * ld_out +
                                                 (int64_t)n_i * BNT);
@@ -519,7 +572,8 @@ namespace {
 
 template <int MODE, int BNT>
 int launch_mode(int ncta, const CUtensorMap& mx, const CUtensorMap& mw, void* out, int M, int N,
-                int K, int64_t ld_out, int band_m, int units, cudaStream_t stream) {
+                int K, int64_t ld_out, int band_m, int units, cudaStream_t stream,
+                const gm::QkvEpi& qe) {
   cudaLaunchConfig_t lc = {};
   cudaLaunchAttribute at[1];
   lc.gridDim = dim3((unsigned)(units * ncta));
@@ -537,23 +591,25 @@ int launch_mode(int ncta, const CUtensorMap& mx, const CUtensorMap& mw, void* ou
     lc.numAttrs = 1;
     lc.dynamicSmemBytes = gm::Cfg<2, BNT>::SMEM;
     CT_CUDA(cudaLaunchKernelEx(&lc, gm::gemm_kernel<2, MODE, BNT>, mx, mw, out, M, N, K, ld_out,
-                               band_m));
+                               band_m, qe));
   } else {
     CT_CUDA(cudaFuncSetAttribute(gm::gemm_kernel<1, MODE, BNT>,
                                  cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)gm::Cfg<1, BNT>::SMEM));
     lc.dynamicSmemBytes = gm::Cfg<1, BNT>::SMEM;
     CT_CUDA(cudaLaunchKernelEx(&lc, gm::gemm_kernel<1, MODE, BNT>, mx, mw, out, M, N, K, ld_out,
-                               band_m));
+                               band_m, qe));
   }
-  return check_launch(MODE == gm::SWIGLU ? "gemm_swiglu_kernel" : "gemm_bf16_kernel");
+  return check_launch(MODE == gm::SWIGLU ? "gemm_swiglu_kernel"
+                      : MODE == gm::QKV  ? "gemm_qkv_rope_kernel"
+                                         : "gemm_bf16_kernel");
 }
 
 // x [M][K] bf16 (row stride ldx) times w [K][wcols] bf16 (row stride ldw);
 // N = activation width (SWIGLU, wcols = 2N) or output columns (wcols = N)
 int launch(int mode, const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
            int64_t wcols, int64_t ldw, int64_t N, void* out, int64_t ld_out, int out_bytes,
-           void* stream) {
+           void* stream, const gm::QkvEpi& qe = gm::QkvEpi{}) {
   if (M < 1 || K < 1 || N < 1)
     return fail(CT_ERR_SHAPE, "gemm geometry M=%lld K=%lld N=%lld", (long long)M, (long long)K,
                 (long long)N);
@@ -582,7 +638,7 @@ int launch(int mode, const void* x, int64_t M, int64_t K, int64_t ldx, const voi
   // the whole A operand from shared memory for half the MACs, and measured
   // 25-33 % slower than 256-wide tiles on the step's projections even where
   // they fill the last wave better (tools/gemm_proj_bench.py)
-  const bool narrow = mode != gm::SWIGLU && N % 256;
+  const bool narrow = mode != gm::SWIGLU && mode != gm::QKV && N % 256;
   const int64_t tiles = mt * (mode == gm::SWIGLU ? N / 128 : N / (narrow ? 128 : 256));
   // M-tiles per band: an A slice of at most ~60 MB (L2 is 126 MB over two
   // dies), bands of equal size.  Standalone (tools/gemm_band_sweep.sh) 40
@@ -602,12 +658,14 @@ int launch(int mode, const void* x, int64_t M, int64_t K, int64_t ldx, const voi
   const cudaStream_t st = (cudaStream_t)stream;
   const int m = (int)M, n = (int)N, k = (int)K;
   if (mode == gm::SWIGLU)
-    return launch_mode<gm::SWIGLU, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st);
+    return launch_mode<gm::SWIGLU, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st, qe);
+  if (mode == gm::QKV)
+    return launch_mode<gm::QKV, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st, qe);
   if (mode == gm::STORE)
-    return narrow ? launch_mode<gm::STORE, 128>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st)
-                  : launch_mode<gm::STORE, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st);
-  return narrow ? launch_mode<gm::ADD, 128>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st)
-                : launch_mode<gm::ADD, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st);
+    return narrow ? launch_mode<gm::STORE, 128>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st, qe)
+                  : launch_mode<gm::STORE, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st, qe);
+  return narrow ? launch_mode<gm::ADD, 128>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st, qe)
+                : launch_mode<gm::ADD, 256>(ncta, mx, mw, out, m, n, k, ld_out, band_m, units, st, qe);
 }
 
 }  // namespace
@@ -625,4 +683,26 @@ extern "C" int ct_gemm_bf16(const void* x, int64_t M, int64_t K, int64_t ldx, co
   if (out_dtype == CT_F32 && accumulate)
     return launch(gm::ADD, x, M, K, ldx, w, N, ldw, N, out, ld_out, 4, stream);
   return fail(CT_ERR_UNSUPPORTED, "gemm_bf16: bf16 store or f32 accumulate only");
+}
+
+// q|k|v projection + RoPE + cache scatter in one kernel (bf16, head_dim 128,
+// adjacent pairing): replaces torch.mm(x, wqkv) -> ct_qkv_rope_scatter.
+extern "C" int ct_gemm_qkv_rope(const void* x, int64_t M, int64_t K, int64_t ldx, const void* w,
+                                int64_t ldw, const int32_t* positions, const void* table,
+                                int64_t Hq, int64_t Hkv, int64_t D, void* q_out, void* k_cache,
+                                void* v_cache, int64_t cache_row_stride, void* stream) {
+  if (D != 128) return fail(CT_ERR_UNSUPPORTED, "gemm_qkv_rope: head_dim %lld != 128", (long long)D);
+  if (Hq < 1 || Hkv < 1 || Hq % Hkv)
+    return fail(CT_ERR_SHAPE, "gemm_qkv_rope: Hq=%lld Hkv=%lld", (long long)Hq, (long long)Hkv);
+  if (!positions || !table || !q_out || !k_cache || !v_cache) return fail(CT_ERR_PARAM, "null tensor");
+  if ((((uintptr_t)table | (uintptr_t)q_out | (uintptr_t)k_cache | (uintptr_t)v_cache) & 15) ||
+      cache_row_stride % 8 || cache_row_stride < Hkv * D)
+    return fail(CT_ERR_UNSUPPORTED, "gemm_qkv_rope needs 16-byte aligned rows");
+  const int64_t N = (Hq + 2 * Hkv) * D;
+  if (N % 256) return fail(CT_ERR_UNSUPPORTED, "gemm_qkv_rope: (Hq + 2 Hkv) must be even");
+  if (M == 0) return CT_OK;
+  gm::QkvEpi qe{positions, static_cast<const float4*>(table), static_cast<__nv_bfloat16*>(q_out),
+                static_cast<__nv_bfloat16*>(k_cache), static_cast<__nv_bfloat16*>(v_cache),
+                cache_row_stride, (int)Hq, (int)Hkv};
+  return launch(gm::QKV, x, M, K, ldx, w, N, ldw, N, q_out, N, 2, stream, qe);
 }

@@ -181,6 +181,9 @@ def _mm_f32(a: torch.Tensor, w: torch.Tensor) -> torch.Tensor:
 # the SM clock (1,470 vs 1,505 MHz) and measured neutral at config 2 (94.9 vs
 # 94.9 ms) and 1 % slower at config 3 (261.5 vs 258.8 ms)
 _GEMM_OWN_ENV = __import__("os").environ.get("CT_GEMM_OWN", "0") == "1"
+# CT_QKV_FUSED=0 (read once): QKV on cuBLAS + the separate ct_qkv_rope_scatter
+# epilogue kernel instead of ct_gemm_qkv_rope (A/B switch)
+_QKV_FUSED_ENV = __import__("os").environ.get("CT_QKV_FUSED", "1") != "0"
 _PAIRS = []
 
 
@@ -269,6 +272,13 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
     wsb = lib.ct_attention_workspace_bytes(a, hq, n_ctx, hkv, d, dtc)
     ws = _dev.workspace(wsb, "attention")
     scale = 1.0 / math.sqrt(d)
+    # bf16 / head_dim 128 / adjacent pairs: q|k|v GEMM with RoPE + cache
+    # scatter in its epilogue (ct_gemm_qkv_rope) over the fused-MLP row range
+    qkv_fused = (_QKV_FUSED_ENV and dt == torch.bfloat16 and d == 128 and not k_raw_out
+                 and params.pairing_code == _lib.CT_ROPE_ADJACENT
+                 and FUSED_MIN_ROWS <= a <= FUSED_MAX_ROWS and (hq + 2 * hkv) % 2 == 0
+                 and hid % 64 == 0 and buf.x.stride(1) == 1
+                 and all(lw["wqkv"].stride(1) == 1 for lw in model.layers))
     _lib.call("ct_embedding_gather", _dev.ptr(model.embedding), _dev.ptr(tokens), a, hid,
               _dev.ptr(buf.h), st)
     _lib.call("ct_residual_rmsnorm", _dev.ptr(buf.h), None, _lib.CT_F32, a, hid, NORM_EPS,
@@ -278,15 +288,24 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
         kc, vc = caches[l]
         if hook is not None:
             hook(l, "start")
-        _proj_mm(buf.qkv, buf.x, w["wqkv"], st)
-        tq = timer.start("qkv") if timer is not None else None
-        _lib.check(lib.ct_qkv_rope_scatter(
-            _dev.ptr(buf.qkv), buf.qkv.shape[1], dtc, _dev.ptr(positions), a, hq, hkv, d,
-            params.pairing_code, _dev.ptr(table), _dev.ptr(buf.q), dtc, _dev.ptr(kc),
-            _dev.ptr(vc), dtc, hkv * d, _dev.ptr(k_raw_out[l]) if k_raw_out else None, st),
-            "ct_qkv_rope_scatter")
-        if timer is not None:
-            timer.stop("qkv", tq)
+        if qkv_fused:
+            wq = w["wqkv"]
+            tq = timer.start("qkv_gemm") if timer is not None else None
+            _lib.call("ct_gemm_qkv_rope", _dev.ptr(buf.x), a, hid, buf.x.stride(0), _dev.ptr(wq),
+                      wq.stride(0), _dev.ptr(positions), _dev.ptr(table), hq, hkv, d,
+                      _dev.ptr(buf.q), _dev.ptr(kc), _dev.ptr(vc), hkv * d, st)
+            if timer is not None:
+                timer.stop("qkv_gemm", tq)
+        else:
+            _proj_mm(buf.qkv, buf.x, w["wqkv"], st)
+            tq = timer.start("qkv") if timer is not None else None
+            _lib.check(lib.ct_qkv_rope_scatter(
+                _dev.ptr(buf.qkv), buf.qkv.shape[1], dtc, _dev.ptr(positions), a, hq, hkv, d,
+                params.pairing_code, _dev.ptr(table), _dev.ptr(buf.q), dtc, _dev.ptr(kc),
+                _dev.ptr(vc), dtc, hkv * d, _dev.ptr(k_raw_out[l]) if k_raw_out else None, st),
+                "ct_qkv_rope_scatter")
+            if timer is not None:
+                timer.stop("qkv", tq)
         if hook is not None:
             hook(l, "recomputed")
         if reuse is not None:
