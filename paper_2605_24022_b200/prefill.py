@@ -273,13 +273,15 @@ def _run_layers(model: GpuModel, tokens: torch.Tensor, positions: torch.Tensor, 
     ws = _dev.workspace(wsb, "attention")
     scale = 1.0 / math.sqrt(d)
     # bf16 / head_dim 128 / adjacent pairs: q|k|v GEMM with RoPE + cache
-    # scatter in its epilogue (ct_gemm_qkv_rope) from FUSED_MIN_ROWS rows up:
-    # 1.09-1.48x over cuBLAS + ct_qkv_rope_scatter from 2,048 to 65,600 rows
-    # (tools/qkv_rows_bench.py, profiles/round2_qkv_rows.txt), so the
-    # full-recompute baseline runs it too
+    # scatter in its epilogue (ct_gemm_qkv_rope) over the fused-MLP row range.
+    # Standalone it is 1.09-1.48x over cuBLAS + ct_qkv_rope_scatter from 2,048
+    # to 65,600 rows (profiles/round2_qkv_rows.txt), but inside the
+    # power-capped 32K-row full prefill it measured 0.8 % slower
+    # (profiles/round2_qkv_full_ab.txt), so, like the MLP, each path runs its
+    # faster form
     qkv_fused = (_QKV_FUSED_ENV and dt == torch.bfloat16 and d == 128 and not k_raw_out
                  and params.pairing_code == _lib.CT_ROPE_ADJACENT
-                 and FUSED_MIN_ROWS <= a and (hq + 2 * hkv) % 2 == 0
+                 and FUSED_MIN_ROWS <= a <= FUSED_MAX_ROWS and (hq + 2 * hkv) % 2 == 0
                  and hid % 64 == 0 and buf.x.stride(1) == 1
                  and all(lw["wqkv"].stride(1) == 1 for lw in model.layers))
     _lib.call("ct_embedding_gather", _dev.ptr(model.embedding), _dev.ptr(tokens), a, hid,
